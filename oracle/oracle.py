@@ -19,6 +19,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBS = {
     "port": (os.path.join(HERE, "liboracle.so"), "ora_"),
     "reference": (os.path.join(HERE, "_ref", "libaggkin_ref.so"), "ref_"),
+    # the restatement built with FMA contraction: the CPU-vs-CPU noise floor for trajectories
+    "port_fma": (os.path.join(HERE, "liboracle_fma.so"), "ora_"),
 }
 
 AGGREGATION, SOURCES, SHATTERING = 0, 1, 2

@@ -1,0 +1,259 @@
+// fft.cuh — fp64 complex FFT building blocks for sm_100a (SIMT DFMA pipe; no tensor cores).
+//
+// Replaces the reference's radix-2 plan (fft.cpp:64-137): instead of one length-P transform
+// with a bit-reversal permutation, transforms are done by teams of threads on-chip:
+//   * each thread holds E points in registers, E in {2,4,8,16};
+//   * Stockham autosort passes (radix <= E) exchange through shared memory, so no
+//     bit-reversal pass and every pass' global/shared traffic is unit-stride;
+//   * radix-16/8/4/2 butterflies are straight-line code with compile-time twiddles; inter-pass
+//     twiddles come from an accurate table (host long-double sincos) in global memory (L1).
+// Layout contract of block_fft: thread j of a team of T = N/E threads holds x[j + r*T] in
+// v[r] on entry and X[j + r*T] on exit (natural order, same distribution).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace agk {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// multiply by exp(SIGN * i*pi/2): SIGN=-1 -> -i (forward), SIGN=+1 -> +i (inverse)
+template <int SIGN>
+__device__ __forceinline__ double2 mul_q(double2 a) {
+  return SIGN < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+// exp(SIGN * 2*pi*i*m/16), m in [0,16): compile-time constants after unrolling.
+template <int SIGN>
+__device__ __forceinline__ double2 w16(int m) {
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  constexpr double h = 0.70710678118654752440;
+  const double cs[16] = {1.0, c1, h, s1, 0.0, -s1, -h, -c1, -1.0, -c1, -h, -s1, 0.0, s1, h, c1};
+  const double sn[16] = {0.0, s1, h, c1, 1.0, c1, h, s1, 0.0, -s1, -h, -c1, -1.0, -c1, -h, -s1};
+  return make_double2(cs[m & 15], SIGN * sn[m & 15]);
+}
+
+// multiply by a compile-time 16th root of unity, using the cheap forms where they exist
+template <int SIGN>
+__device__ __forceinline__ double2 mul_w16(double2 a, int m) {
+  m &= 15;
+  if (m == 0) return a;
+  if (m == 4) return mul_q<SIGN>(a);
+  if (m == 8) return make_double2(-a.x, -a.y);
+  if (m == 12) return mul_q<-SIGN>(a);
+  if (m == 2 || m == 6 || m == 10 || m == 14) {  // (+-1 +- i)/sqrt2
+    constexpr double h = 0.70710678118654752440;
+    const double2 w = w16<SIGN>(m);
+    // (x+iy)(wr+i wi) with |wr|=|wi|=h
+    return make_double2(h * ((w.x > 0 ? a.x : -a.x) - (w.y > 0 ? a.y : -a.y)),
+                        h * ((w.y > 0 ? a.x : -a.x) + (w.x > 0 ? a.y : -a.y)));
+  }
+  return cmul(a, w16<SIGN>(m));
+}
+
+// ---- in-register DFTs, natural order in and out
+template <int R, int SIGN>
+struct Dft;
+
+template <int SIGN>
+struct Dft<1, SIGN> {
+  __device__ __forceinline__ static void run(double2*) {}
+};
+
+template <int SIGN>
+struct Dft<2, SIGN> {
+  __device__ __forceinline__ static void run(double2* x) {
+    const double2 a = x[0];
+    x[0] = cadd(a, x[1]);
+    x[1] = csub(a, x[1]);
+  }
+};
+
+template <int SIGN>
+struct Dft<4, SIGN> {
+  __device__ __forceinline__ static void run(double2* x) {
+    const double2 s02 = cadd(x[0], x[2]), d02 = csub(x[0], x[2]);
+    const double2 s13 = cadd(x[1], x[3]), d13 = mul_q<SIGN>(csub(x[1], x[3]));
+    x[0] = cadd(s02, s13);
+    x[2] = csub(s02, s13);
+    x[1] = cadd(d02, d13);
+    x[3] = csub(d02, d13);
+  }
+};
+
+// radix-2 decimation in time on top of the half-size DFT: X[k] = E[k] + W^k O[k]
+template <int R, int SIGN>
+struct Dft {
+  __device__ __forceinline__ static void run(double2* x) {
+    double2 e[R / 2], o[R / 2];
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) {
+      e[r] = x[2 * r];
+      o[r] = x[2 * r + 1];
+    }
+    Dft<R / 2, SIGN>::run(e);
+    Dft<R / 2, SIGN>::run(o);
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      const double2 t = mul_w16<SIGN>(o[k], k * (16 / R));
+      x[k] = cadd(e[k], t);
+      x[k + R / 2] = csub(e[k], t);
+    }
+  }
+};
+
+// DFT of R points whose upper half is zero (zero-padded convolution input):
+// X[2k] = DFT_{R/2}(x)[k], X[2k+1] = DFT_{R/2}(x_r W_R^r)[k].
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_halfzero(double2* x) {
+  if constexpr (R == 1) {
+    return;
+  } else {
+    double2 a[R / 2], b[R / 2];
+#pragma unroll
+    for (int r = 0; r < R / 2; ++r) {
+      a[r] = x[r];
+      b[r] = mul_w16<SIGN>(x[r], r * (16 / R));
+    }
+    Dft<R / 2, SIGN>::run(a);
+    Dft<R / 2, SIGN>::run(b);
+#pragma unroll
+    for (int k = 0; k < R / 2; ++k) {
+      x[2 * k] = a[k];
+      x[2 * k + 1] = b[k];
+    }
+  }
+}
+
+__host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
+
+// Shared-memory index padding: one spare slot every 2^S entries breaks the bank conflicts of
+// the radix-2^S first pass (stride 2^S x 16 B).
+template <int S>
+__device__ __forceinline__ int pad_idx(int i) {
+  return i + (i >> S);
+}
+template <int N, int S>
+struct Padded {
+  static constexpr int value = N + (N >> S) + 1;  // +1: successive team regions start on different banks
+};
+
+// Accurate table of W_NT^k = exp(-2*pi*i*k/NT), k < NT, NT a power of two >= N.
+struct TwTable {
+  const double2* w;
+  int log2n;
+};
+
+template <int SIGN>
+__device__ __forceinline__ double2 tw_lookup(const TwTable& t, int k) {
+  const double2 w = __ldg(t.w + k);
+  return SIGN < 0 ? w : cconj(w);
+}
+
+// One Stockham pass of radix R over a team's data (see file header for the layout).
+template <int N, int E, int R, int SIGN, int PADS, bool LAST, bool HALFZERO>
+__device__ __forceinline__ void stockham_pass(double2 (&v)[E], double2* sm, int j, int ns,
+                                              const TwTable& tw, bool active) {
+  constexpr int T = N / E;
+  constexpr int Q = E / R;
+  if (active) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int b = j + q * T;
+      const int k = b & (ns - 1);
+      double2 u[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
+      if (ns > 1) {
+        // W_{ns*R}^{k*r} = W_NT^{k*r*NT/(ns*R)}
+        const int shift = tw.log2n - ilog2(R) - (31 - __clz(ns));
+#pragma unroll
+        for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw_lookup<SIGN>(tw, (k * r) << shift));
+      }
+      if constexpr (HALFZERO) {
+        dft_halfzero<R, SIGN>(u);
+      } else {
+        Dft<R, SIGN>::run(u);
+      }
+      if constexpr (LAST) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[q + r * Q] = u[r];
+      } else {
+        const int base = (b - k) * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[pad_idx<PADS>(base + r * ns)] = u[r];
+      }
+    }
+  }
+  if constexpr (!LAST) {
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = sm[pad_idx<PADS>(j + r * T)];
+    }
+    __syncthreads();
+  }
+}
+
+// Pass schedule: first pass radix = 2^(log2N mod log2E) if nonzero (so that the Ns=1 pass,
+// which carries the zero-padding, can be the small one), then passes of radix E.
+template <int N, int E>
+struct FftPlan {
+  static constexpr int L = ilog2(N), LE = ilog2(E);
+  static constexpr int REM = L % LE;
+  static constexpr int R0 = REM ? (1 << REM) : E;  // radix of the first (Ns = 1) pass
+  static constexpr int NFULL = REM ? L / LE : L / LE - 1;  // radix-E passes after the first
+  static constexpr int PADS = ilog2(R0) > 0 ? ilog2(R0) : 1;
+  static constexpr int SMEM = Padded<N, PADS>::value;  // double2 entries per team
+};
+
+template <int N, int E, int SIGN, int PADS, int IDX, int NPASS>
+struct FullPasses {
+  __device__ __forceinline__ static void run(double2 (&v)[E], double2* sm, int j, int ns,
+                                             const TwTable& tw, bool active) {
+    if constexpr (IDX < NPASS) {
+      stockham_pass<N, E, E, SIGN, PADS, IDX == NPASS - 1, false>(v, sm, j, ns, tw, active);
+      FullPasses<N, E, SIGN, PADS, IDX + 1, NPASS>::run(v, sm, j, ns * E, tw, active);
+    }
+  }
+};
+
+// N-point FFT by a team of N/E threads (team-local smem region `sm`, FftPlan::SMEM entries).
+// Every thread of the CTA must call it (barriers); inactive threads pass active=false.
+// HALFZERO: entries x[N/2..N) are zero on entry (v[r] for r >= E/2 are ignored).
+template <int N, int E, int SIGN, bool HALFZERO>
+__device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, const TwTable& tw,
+                                          bool active = true) {
+  using P = FftPlan<N, E>;
+  static_assert(E <= N, "E must not exceed N");
+  if constexpr (N == 1) {
+    return;
+  } else {
+    constexpr bool only = (P::NFULL == 0);
+    stockham_pass<N, E, P::R0, SIGN, P::PADS, only, HALFZERO>(v, sm, j, 1, tw, active);
+    FullPasses<N, E, SIGN, P::PADS, 0, P::NFULL>::run(v, sm, j, P::R0, tw, active);
+  }
+}
+
+// W_P^e for the four-step twiddles, e < P, from two short tables:
+// W_P^e = hi[e >> s] * lo[e & (2^s - 1)].
+struct TwoLevel {
+  const double2* hi;
+  const double2* lo;
+  int s;
+};
+template <int SIGN>
+__device__ __forceinline__ double2 tw_p(const TwoLevel& t, uint32_t e) {
+  const double2 a = __ldg(t.hi + (e >> t.s));
+  const double2 b = __ldg(t.lo + (e & ((1u << t.s) - 1u)));
+  const double2 w = cmul(a, b);
+  return SIGN < 0 ? w : cconj(w);
+}
+
+}  // namespace agk

@@ -1,0 +1,87 @@
+// internal.h — device-side parameter blocks shared by the RHS, stepper and API translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "agk/agk.h"
+#include "fft.cuh"
+
+namespace agk {
+
+// Epilogue terms (eval_rhs = birth - death [+ sources | + shattering]); the term-level entry
+// points birth_term / death_term / shattering_terms select subsets.
+enum TermFlags : int {
+  T_BIRTH = 1,       // + 0.5 * conv
+  T_DEATH = 2,       // - n_s * rowsum_s
+  T_DEATH_POS = 4,   // + n_s * rowsum_s (death_term's own sign)
+  T_SOURCES = 8,     // + P_k at k-1
+  T_SHATTER = 16,    // shattering terms with lambda
+};
+
+// Device addresses of the state vector an RHS reads: n + (*sel) * sel_stride when sel != null
+// (the run loop double-buffers the state and flips an index instead of copying).
+struct VecRef {
+  const double* base;
+  const int* sel;
+  int64_t stride;
+  __device__ __forceinline__ const double* get() const { return sel ? base + (*sel) * stride : base; }
+};
+
+// Everything an RHS evaluation needs, by value in every kernel.
+struct RhsArgs {
+  VecRef n;             // input state (m)
+  double* out;          // output S(n) (m)
+  const int* skip;      // if non-null and *skip != 0 the whole evaluation is skipped
+  int64_t m;
+  int r;                // all ranks
+  int rf;               // unique ranks (FFT count)
+  const double* ut;     // r x m: U transposed (ut[a*m + i] = U(i+1, a))
+  const double* v;      // r x m: V as in the reference
+  const int* uniq_rank; // rf: original rank index of unique rank ub
+  const double* uniq_weight; // rf: fold weight (1 + number of folded copies)
+  const int* rank_map;  // r: unique index of rank a, +1000000 if folded swapped
+  const double* u0;     // r: U(1, a)
+  const double* v0;     // r: V(a, 1)
+  int flags;            // TermFlags
+  double lambda;
+  const int64_t* src_k; // 1-based
+  const double* src_rate;
+  int nsrc;
+  // four-step geometry
+  int log2p;
+  int n1, n2;           // P = n1 * n2
+  // scratch
+  double2* y;           // group intermediate (gsize * P)
+  double2* acc;         // (n1/2 + 1) * n2 accumulator, then G rows
+  double* partials;     // rf * nblk_colfwd * 4
+  double* scalars;      // r (w_a) + 2 (pair_gain, mono_gain)
+  int nblk_colfwd;
+  TwTable tw_n1, tw_n2, tw_small;
+  TwoLevel twp;
+};
+
+// Launch geometry and per-handle tables for one problem size.
+struct RhsPlan {
+  int small;     // 1: single-CTA path (P <= 8192)
+  int log2p;
+  int n1, n2, c, cp;
+  int gsize;     // ranks per group in the four-step path
+  int launches;  // kernels per RHS
+};
+
+// host-side launchers (rhs.cu)
+void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);
+cudaError_t rhs_launch(const RhsPlan& plan, const RhsArgs& a, cudaStream_t s);
+size_t rhs_y_elems(const RhsPlan& plan);
+size_t rhs_acc_elems(const RhsPlan& plan);
+size_t rhs_partial_elems(const RhsPlan& plan, int rf);
+cudaError_t rhs_set_smem_limits();
+
+// Injected fakes (AGK_RHS_DECAY, ...) as one elementwise kernel.
+cudaError_t fake_rhs_launch(int kind, double param, VecRef n, double* out, int64_t m,
+                            const int* skip, cudaStream_t s);
+
+}  // namespace agk

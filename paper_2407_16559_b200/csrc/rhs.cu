@@ -1,0 +1,578 @@
+// rhs.cu — B200 kernels for the low-rank Smoluchowski right-hand side (fp64, sm_100a).
+//
+// Replaces eval_rhs / birth_term / death_term / shattering_terms (reference src/rhs.cpp:24-235).
+// The reference does, per unique rank, one packed length-P complex FFT of z = U_a n + i V_a n,
+// splits the two real spectra, accumulates w * A_k B_k, then one inverse FFT (rhs.cpp:126-149),
+// and separately R dot products + an M x R pass for the death term (rhs.cpp:24-36).
+//
+// Here the same algebra runs as
+//   small path (P = next_pow2(2m) <= 8192): ONE CTA does everything on-chip (k_small);
+//   four-step path (P = N1 * N2 >= 2^14), per group of unique ranks:
+//     k_col_fwd : fused load of U_a∘n and V_a∘n (zero padding never materialised), N1-point
+//                 column FFTs in registers/smem, four-step twiddle, moment partials
+//                 (w_a and the shattering sums) -> intermediate Y (L2 resident per group)
+//     k_row     : row FFTs of rows k1 and N1-k1 together, conjugate-pair split, w*A*B summed
+//                 over the group's ranks in registers; the last group also does the inverse
+//                 row FFT of the Hermitian half (rows 0..N1/2) and the inverse twiddle -> G
+//   then k_col_inv : two real columns per complex inverse FFT (G is Hermitian in k1), 1/P and
+//                 the 1/2 of the birth term, death (n_s * sum_a U_sa w_a), sources and
+//                 shattering fused into the epilogue -> out.
+// All reductions are fixed-order (no floating-point atomics): results are bitwise
+// reproducible run to run.
+#include <cstdio>
+
+#include "internal.h"
+
+namespace agk {
+
+constexpr int kSwap = 1000000;  // rank_map code offset for swapped folds
+
+// ------------------------------------------------------------------ shared device helpers
+
+// Sum NV doubles over the CTA (fixed shuffle tree + fixed warp order); result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&x)[NV], double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x[k] += __shfl_xor_sync(0xffffffffu, x[k], off);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[warp * NV + k] = x[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < nw; ++w) s += red[w * NV + k];
+      x[k] = s;
+    }
+  }
+  __syncthreads();
+}
+
+// Reduce the per-CTA moment partials [ub][blk][4] into tot[ub*4+q] (global scratch), fixed
+// order, by all warps of the calling CTA (blockDim a multiple of 32).
+__device__ void reduce_partials(const RhsArgs& a, int nblk, double* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int p = warp; p < a.rf * 4; p += nw) {
+    const int ub = p >> 2, q = p & 3;
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += a.partials[((int64_t)ub * nblk + b) * 4 + q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) tot[p] = s;
+  }
+}
+
+// w_a for every rank (folded ranks read their partner's sums), pair and monomer gains
+// (rhs.cpp:24-36 and 185-196), written to a.scalars by one thread.
+__device__ void finalize_scalars(const RhsArgs& a, const double* tot, double n0) {
+  double pair = 0.0, mono = 0.0;
+  for (int ra = 0; ra < a.r; ++ra) {
+    const int code = a.rank_map[ra];
+    const bool sw = code >= kSwap;
+    const int ub = sw ? code - kSwap : code;
+    const double A0 = tot[ub * 4 + 0], A1 = tot[ub * 4 + 1];
+    const double B0 = tot[ub * 4 + 2], B1 = tot[ub * 4 + 3];
+    const double su0 = sw ? B0 : A0, su1 = sw ? B1 : A1;
+    const double sv0 = sw ? A0 : B0, sv1 = sw ? A1 : B1;
+    a.scalars[ra] = sv0 + a.v0[ra] * n0;  // w_a = sum_j V_aj n_j
+    pair += su1 * sv0 + su0 * sv1;
+    mono += a.u0[ra] * sv1;
+  }
+  a.scalars[a.r] = pair;
+  a.scalars[a.r + 1] = mono;
+}
+
+// Epilogue for output index jo >= 1: S = birth - death [+ shattering loss] [+ sources]
+__device__ __forceinline__ double epilogue(const RhsArgs& a, const double* __restrict__ n,
+                                           int64_t jo, double birth) {
+  double res = (a.flags & T_BIRTH) ? birth : 0.0;
+  if (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) {
+    double rowsum = 0.0;
+    for (int ra = 0; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + jo) * __ldg(a.scalars + ra);
+    const double nn = n[jo];
+    if (a.flags & T_DEATH) res = res - nn * rowsum;
+    if (a.flags & T_DEATH_POS) res = nn * rowsum;
+    if (a.flags & T_SHATTER) res = res + (-a.lambda * nn) * rowsum;
+  }
+  if (a.flags & T_SOURCES) {
+    for (int q = 0; q < a.nsrc; ++q)
+      if (a.src_k[q] - 1 == jo) res += a.src_rate[q];
+  }
+  return res;
+}
+
+// out[0]: no birth; death; shattering gain at s = 1 (rhs.cpp:208); sources at k = 1.
+__device__ __forceinline__ double epilogue0(const RhsArgs& a, const double* __restrict__ n) {
+  double res = 0.0;
+  const double n0 = n[0];
+  if (a.flags & (T_DEATH | T_DEATH_POS)) {
+    double rowsum = 0.0;
+    for (int ra = 0; ra < a.r; ++ra) rowsum += a.ut[(int64_t)ra * a.m] * a.scalars[ra];
+    if (a.flags & T_DEATH) res = res - n0 * rowsum;
+    if (a.flags & T_DEATH_POS) res = n0 * rowsum;
+  }
+  if (a.flags & T_SHATTER) {
+    const double pair = a.scalars[a.r], mono = a.scalars[a.r + 1];
+    res = res + (0.5 * a.lambda * pair + a.lambda * n0 * mono);
+  }
+  if (a.flags & T_SOURCES) {
+    for (int q = 0; q < a.nsrc; ++q)
+      if (a.src_k[q] == 1) res += a.src_rate[q];
+  }
+  return res;
+}
+
+// conjugate-pair split and product of one packed spectrum bin (rhs.cpp:138-144):
+// A = (Z + conj Zp)/2, B = -i/2 (Z - conj Zp), returns A*B
+__device__ __forceinline__ double2 split_product(double2 z, double2 zp) {
+  const double mr = zp.x, mi = -zp.y;
+  const double ar = 0.5 * (z.x + mr), ai = 0.5 * (z.y + mi);
+  const double dr = z.x - mr, di = z.y - mi;
+  const double br = 0.5 * di, bi = -0.5 * dr;
+  return make_double2(ar * br - ai * bi, ar * bi + ai * br);
+}
+
+// ------------------------------------------------------------------ small path: one CTA
+
+template <int P>
+struct SmallCfg {
+  static constexpr int E = P >= 16 ? 16 : P;
+  static constexpr int T = P / E;
+  static constexpr int NT = T < 128 ? 128 : T;
+};
+
+template <int P>
+__global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
+  using CF = SmallCfg<P>;
+  constexpr int E = CF::E, T = CF::T, NT = CF::NT;
+  using PL = FftPlan<P, E>;
+  constexpr int H = P / 2 + 1;
+  constexpr int QA = (H + NT - 1) / NT;
+  extern __shared__ double2 zs[];
+  __shared__ double red[(NT / 32) * 4];
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x;
+  const int64_t m = a.m;
+  const double* __restrict__ n = a.n.get();
+  const bool act = tid < T;
+  double2 acc[QA];
+#pragma unroll
+  for (int q = 0; q < QA; ++q) acc[q] = czero();
+
+  for (int ub = 0; ub < a.rf; ++ub) {
+    const int ra = a.uniq_rank[ub];
+    const double* __restrict__ ut = a.ut + (int64_t)ra * m;
+    const double* __restrict__ vv = a.v + (int64_t)ra * m;
+    const double wt = a.uniq_weight[ub];
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = tid; i < P; i += NT) {
+      double2 z = czero();
+      if (i < m) {
+        const double ni = n[i];
+        z = make_double2(ut[i] * ni, vv[i] * ni);
+        if (i >= 1) {
+          const double sz = (double)(i + 1);
+          s[0] += z.x;
+          s[1] += sz * z.x;
+          s[2] += z.y;
+          s[3] += sz * z.y;
+        }
+      }
+      zs[pad_idx<PL::PADS>(i)] = z;
+    }
+    block_sum<4>(s, red);
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a.partials[ub * 4 + q] = s[q];
+    }
+    double2 v[E];
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < E; ++r) v[r] = zs[pad_idx<PL::PADS>(tid + r * T)];
+    }
+    __syncthreads();
+    block_fft<P, E, -1, false>(v, zs, tid, a.tw_small, act);
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < E; ++r) zs[pad_idx<PL::PADS>(tid + r * T)] = v[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < QA; ++q) {
+      const int k = tid + q * NT;
+      if (k < H) {
+        const double2 pr = split_product(zs[pad_idx<PL::PADS>(k)], zs[pad_idx<PL::PADS>((P - k) & (P - 1))]);
+        acc[q].x += wt * pr.x;
+        acc[q].y += wt * pr.y;
+      }
+    }
+    __syncthreads();
+  }
+  // Hermitian spectrum of the real convolution, then one inverse transform
+#pragma unroll
+  for (int q = 0; q < QA; ++q) {
+    const int k = tid + q * NT;
+    if (k < H) {
+      zs[pad_idx<PL::PADS>(k)] = acc[q];
+      if (k > 0 && k < P / 2) zs[pad_idx<PL::PADS>(P - k)] = cconj(acc[q]);
+    }
+  }
+  __syncthreads();
+  double2 v[E];
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) v[r] = zs[pad_idx<PL::PADS>(tid + r * T)];
+  }
+  __syncthreads();
+  block_fft<P, E, +1, false>(v, zs, tid, a.tw_small, act);
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < E; ++r) zs[pad_idx<PL::PADS>(tid + r * T)] = v[r];
+  }
+  if (tid == 0) finalize_scalars(a, a.partials, n[0]);
+  __syncthreads();
+  const double scale = ldexp(0.5, -a.log2p);  // (1/P) of the inverse times the 1/2 of birth
+  for (int64_t jo = tid; jo < m; jo += NT) {
+    if (jo == 0) {
+      a.out[0] = epilogue0(a, n);
+    } else {
+      a.out[jo] = epilogue(a, n, jo, scale * zs[pad_idx<PL::PADS>((int)jo - 1)].x);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ four-step path
+
+template <int L>
+struct Cfg {
+  static constexpr int N1 = 1 << (L / 2), N2 = 1 << (L - L / 2);
+  static constexpr int E1 = N1 >= 256 ? 16 : 8;
+  static constexpr int E2 = N2 >= 256 ? 16 : 8;
+  static constexpr int C = L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 4));
+  static constexpr int CP = C / 2 > 0 ? C / 2 : 1;
+  static constexpr int T1 = N1 / E1, T2 = N2 / E2;
+};
+
+template <int N1, int E1, int C>
+__global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int gcount) {
+  using PL = FftPlan<N1, E1>;
+  constexpr int T1 = N1 / E1;
+  extern __shared__ double2 smem[];
+  __shared__ double red[((C * T1 + 31) / 32) * 4];
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x, c = tid % C, j = tid / C;
+  const int64_t n2 = (int64_t)blockIdx.x * C + c;
+  const int64_t N2 = a.n2, m = a.m, P = (int64_t)N1 * N2;
+  const double* __restrict__ n = a.n.get();
+  double nl[E1 / 2];
+#pragma unroll
+  for (int r = 0; r < E1 / 2; ++r) {
+    const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
+    nl[r] = i < m ? n[i] : 0.0;
+  }
+  double2* sm = smem + c * PL::SMEM;
+  for (int g = 0; g < gcount; ++g) {
+    const int ub = g0 + g;
+    const int ra = a.uniq_rank[ub];
+    const double* __restrict__ ut = a.ut + (int64_t)ra * m;
+    const double* __restrict__ vv = a.v + (int64_t)ra * m;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    double2 v[E1];
+#pragma unroll
+    for (int r = 0; r < E1 / 2; ++r) {
+      const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
+      v[r] = czero();
+      if (i < m) {
+        const double x = __ldg(ut + i) * nl[r], y = __ldg(vv + i) * nl[r];
+        v[r] = make_double2(x, y);
+        if (i >= 1) {
+          const double sz = (double)(i + 1);
+          s[0] += x;
+          s[1] += sz * x;
+          s[2] += y;
+          s[3] += sz * y;
+        }
+      }
+    }
+#pragma unroll
+    for (int r = E1 / 2; r < E1; ++r) v[r] = czero();
+    block_fft<N1, E1, -1, true>(v, sm, j, a.tw_n1);
+    double2* __restrict__ yg = a.y + (int64_t)g * P;
+#pragma unroll
+    for (int r = 0; r < E1; ++r) {
+      const int64_t k1 = j + r * T1;
+      yg[k1 * N2 + n2] = cmul(v[r], tw_p<-1>(a.twp, (uint32_t)(n2 * k1)));
+    }
+    block_sum<4>(s, red);
+    if (tid == 0) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a.partials[((int64_t)ub * a.nblk_colfwd + blockIdx.x) * 4 + q] = s[q];
+    }
+  }
+}
+
+template <int N2, int E2>
+__global__ void __launch_bounds__(2 * (N2 / E2)) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
+  using PL = FftPlan<N2, E2>;
+  constexpr int T2 = N2 / E2, NT = 2 * T2, Q = E2 / 2;
+  using PLI = FftPlan<N2, Q>;
+  extern __shared__ double2 smem[];
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x, team = tid / T2, j = tid % T2;
+  const int n1 = a.n1;
+  const int k1 = blockIdx.x;
+  const int row = team == 0 ? k1 : (n1 - k1) & (n1 - 1);
+  const int64_t P = (int64_t)n1 * N2;
+
+  if (last && blockIdx.x == 0) {
+    double* tot = a.scalars + a.r + 2;
+    reduce_partials(a, a.nblk_colfwd, tot);
+    __syncthreads();
+    if (tid == 0) finalize_scalars(a, tot, a.n.get()[0]);
+  }
+
+  double2 acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = first ? czero() : a.acc[(int64_t)k1 * N2 + tid + q * NT];
+
+  double2* smt = smem + team * PL::SMEM;
+  for (int g = 0; g < gcount; ++g) {
+    const double wt = a.uniq_weight[g0 + g];
+    const double2* __restrict__ yr = a.y + (int64_t)g * P + (int64_t)row * N2;
+    double2 v[E2];
+#pragma unroll
+    for (int r = 0; r < E2; ++r) v[r] = yr[j + r * T2];
+    block_fft<N2, E2, -1, false>(v, smt, j, a.tw_n2);
+#pragma unroll
+    for (int r = 0; r < E2; ++r) smt[pad_idx<PL::PADS>(j + r * T2)] = v[r];
+    __syncthreads();
+    const double2* s0 = smem;
+    const double2* s1 = (k1 == 0) ? smem : smem + PL::SMEM;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int k2 = tid + q * NT;
+      const int pk = (k1 == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
+      const double2 pr = split_product(s0[pad_idx<PL::PADS>(k2)], s1[pad_idx<PL::PADS>(pk)]);
+      acc[q].x += wt * pr.x;
+      acc[q].y += wt * pr.y;
+    }
+    __syncthreads();
+  }
+  if (!last) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) a.acc[(int64_t)k1 * N2 + tid + q * NT] = acc[q];
+    return;
+  }
+  // inverse row transform of the Hermitian half-row k1, then the inverse four-step twiddle
+#pragma unroll
+  for (int q = 0; q < Q; ++q) smem[pad_idx<PLI::PADS>(tid + q * NT)] = acc[q];
+  __syncthreads();
+  double2 u[Q];
+#pragma unroll
+  for (int r = 0; r < Q; ++r) u[r] = smem[pad_idx<PLI::PADS>(tid + r * NT)];
+  __syncthreads();
+  block_fft<N2, Q, +1, false>(u, smem, tid, a.tw_n2);
+#pragma unroll
+  for (int r = 0; r < Q; ++r) {
+    const int64_t c2 = tid + r * NT;
+    a.acc[(int64_t)k1 * N2 + c2] = cmul(u[r], tw_p<+1>(a.twp, (uint32_t)(c2 * k1)));
+  }
+}
+
+template <int N1, int E1, int CP>
+__global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
+  using PL = FftPlan<N1, E1>;
+  constexpr int T1 = N1 / E1;
+  extern __shared__ double2 smem[];
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x, c = tid % CP, j = tid / CP;
+  const int64_t N2 = a.n2, m = a.m;
+  const int64_t col = (int64_t)blockIdx.x * 2 * CP + 2 * c;
+  const double2* __restrict__ G = a.acc;
+  double2 v[E1];
+#pragma unroll
+  for (int r = 0; r < E1; ++r) {
+    const int k1 = j + r * T1;
+    const bool refl = k1 > N1 / 2;
+    const int64_t rowi = refl ? N1 - k1 : k1;
+    double2 ga = G[rowi * N2 + col], gb = G[rowi * N2 + col + 1];
+    if (refl) {
+      ga = cconj(ga);
+      gb = cconj(gb);
+    }
+    v[r] = make_double2(ga.x - gb.y, ga.y + gb.x);  // G_a + i G_b: two real outputs at once
+  }
+  block_fft<N1, E1, +1, false>(v, smem + c * PL::SMEM, j, a.tw_n1);
+  const double* __restrict__ n = a.n.get();
+  const double scale = ldexp(0.5, -a.log2p);
+#pragma unroll
+  for (int r = 0; r < E1 / 2; ++r) {
+    const int64_t base = (int64_t)(j + r * T1) * N2 + col + 1;  // out index = conv index + 1
+    if (base < m) a.out[base] = epilogue(a, n, base, scale * v[r].x);
+    if (base + 1 < m) a.out[base + 1] = epilogue(a, n, base + 1, scale * v[r].y);
+  }
+  if (blockIdx.x == 0 && tid == 0) a.out[0] = epilogue0(a, n);
+}
+
+// ------------------------------------------------------------------ injected fakes
+
+__global__ void k_fake(int kind, double param, VecRef nref, double* out, int64_t m, const int* skip) {
+  if (skip && *skip) return;
+  const double* n = nref.get();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double o;
+    switch (kind) {
+      case AGK_RHS_DECAY: o = -n[i]; break;
+      case AGK_RHS_STILL: o = 0.0; break;
+      case AGK_RHS_DRAIN: o = i == 0 ? -param : 0.0; break;
+      case AGK_RHS_BURST_INF: o = __longlong_as_double(0x7ff0000000000000LL); break;
+      default: o = __longlong_as_double(0x7ff8000000000000LL); break;
+    }
+    out[i] = o;
+  }
+}
+
+cudaError_t fake_rhs_launch(int kind, double param, VecRef n, double* out, int64_t m, const int* skip,
+                            cudaStream_t s) {
+  const int threads = 256;
+  int blocks = (int)((m + threads - 1) / threads);
+  if (blocks > 4 * 148) blocks = 4 * 148;
+  k_fake<<<blocks, threads, 0, s>>>(kind, param, n, out, m, skip);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ host-side dispatch
+
+static int ilog2_host(int64_t x) {
+  int l = 0;
+  while (((int64_t)1 << l) < x) ++l;
+  return l;
+}
+
+void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
+  int64_t P = 1;
+  while (P < 2 * m) P <<= 1;
+  p->log2p = ilog2_host(P);
+  p->small = P <= 8192;
+  p->n1 = 1 << (p->log2p / 2);
+  p->n2 = 1 << (p->log2p - p->log2p / 2);
+  const int L = p->log2p;
+  p->c = L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 4));
+  p->cp = p->c / 2 > 0 ? p->c / 2 : 1;
+  // Ranks per group: keep the group intermediate (16 B x P per rank) well inside the 126 MB L2.
+  int g = (int)((48ll << 20) / (16 * P));
+  if (const char* env = getenv("AGK_RANK_GROUP")) g = atoi(env);
+  if (g < 1) g = 1;
+  if (g > rf) g = rf;
+  p->gsize = g;
+  const int ngroups = (rf + g - 1) / g;
+  p->launches = p->small ? 1 : 2 * ngroups + 1;
+}
+
+size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
+size_t rhs_acc_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)(p.n1 / 2 + 1) * p.n2; }
+size_t rhs_partial_elems(const RhsPlan& p, int rf) {
+  const size_t nblk = p.small ? 1 : (size_t)(p.n2 / p.c);
+  return (size_t)rf * nblk * 4;
+}
+
+template <int P>
+static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s) {
+  using PL = FftPlan<P, SmallCfg<P>::E>;
+  k_small<P><<<1, SmallCfg<P>::NT, PL::SMEM * sizeof(double2), s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int L>
+static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s) {
+  using CF = Cfg<L>;
+  RhsArgs a = a0;
+  a.nblk_colfwd = CF::N2 / CF::C;
+  const size_t sm1 = (size_t)CF::C * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2);
+  const size_t sm2 = (size_t)2 * FftPlan<CF::N2, CF::E2>::SMEM * sizeof(double2);
+  const size_t sm3 = (size_t)CF::CP * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2);
+  for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
+    const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
+    k_col_fwd<CF::N1, CF::E1, CF::C><<<CF::N2 / CF::C, CF::C * CF::T1, sm1, s>>>(a, g0, gc);
+    k_row<CF::N2, CF::E2><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
+  }
+  k_col_inv<CF::N1, CF::E1, CF::CP><<<CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t rhs_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s) {
+  switch (p.log2p) {
+    case 2: return launch_small<4>(a, s);
+    case 3: return launch_small<8>(a, s);
+    case 4: return launch_small<16>(a, s);
+    case 5: return launch_small<32>(a, s);
+    case 6: return launch_small<64>(a, s);
+    case 7: return launch_small<128>(a, s);
+    case 8: return launch_small<256>(a, s);
+    case 9: return launch_small<512>(a, s);
+    case 10: return launch_small<1024>(a, s);
+    case 11: return launch_small<2048>(a, s);
+    case 12: return launch_small<4096>(a, s);
+    case 13: return launch_small<8192>(a, s);
+    case 14: return launch_four_step<14>(p, a, s);
+    case 15: return launch_four_step<15>(p, a, s);
+    case 16: return launch_four_step<16>(p, a, s);
+    case 17: return launch_four_step<17>(p, a, s);
+    case 18: return launch_four_step<18>(p, a, s);
+    case 19: return launch_four_step<19>(p, a, s);
+    case 20: return launch_four_step<20>(p, a, s);
+    case 21: return launch_four_step<21>(p, a, s);
+    case 22: return launch_four_step<22>(p, a, s);
+    case 23: return launch_four_step<23>(p, a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int P>
+static cudaError_t smem_small() {
+  using PL = FftPlan<P, SmallCfg<P>::E>;
+  return cudaFuncSetAttribute(k_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(PL::SMEM * sizeof(double2)));
+}
+
+template <int L>
+static cudaError_t smem_four_step() {
+  using CF = Cfg<L>;
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k_col_fwd<CF::N1, CF::E1, CF::C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(CF::C * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2)));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * FftPlan<CF::N2, CF::E2>::SMEM * sizeof(double2)));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(CF::CP * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2)));
+}
+
+cudaError_t rhs_set_smem_limits() {
+  cudaError_t e = cudaSuccess;
+#define AGK_TRY(x) \
+  if ((e = (x)) != cudaSuccess) return e;
+  AGK_TRY(smem_small<4096>());
+  AGK_TRY(smem_small<8192>());
+  AGK_TRY(smem_four_step<14>());
+  AGK_TRY(smem_four_step<15>());
+  AGK_TRY(smem_four_step<16>());
+  AGK_TRY(smem_four_step<17>());
+  AGK_TRY(smem_four_step<18>());
+  AGK_TRY(smem_four_step<19>());
+  AGK_TRY(smem_four_step<20>());
+  AGK_TRY(smem_four_step<21>());
+  AGK_TRY(smem_four_step<22>());
+  AGK_TRY(smem_four_step<23>());
+#undef AGK_TRY
+  return e;
+}
+
+}  // namespace agk

@@ -1,0 +1,254 @@
+"""GPU parity of the RHS operator through the C ABI against the CPU oracle (reference
+eval_rhs / birth_term / death_term / shattering_terms, rhs.cpp:24-235).
+
+Tolerance: normwise relative error max|got-want|/max|want| <= 1e-11 (north_star; the
+reference's own low-rank vs dense bar is 1e-12, test_rhs.cpp:190) and exact zeros where the
+reference produces exact zeros.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.helpers import config4_inputs, factors, rel_max_diff
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-11
+KERNELS = [("constant", 0.0), ("brownian", 1.0 / 3.0), ("brownian", 0.95), ("brownian2", 0.0)]
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def make(agk, kind, m, alpha=0.0, variant=O.AGGREGATION, sources=(), lam=0.0):
+    u, v = factors(kind, m, alpha)
+    om = O.Model(u, v, variant, list(sources), lam)
+    gm = agk.Model(u, v, variant, list(sources), lam)
+    return om, agk.RhsWorkspace(gm)
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 16, 40, 64, 96, 257, 1000, 2048, 4096])
+@pytest.mark.parametrize("kind,alpha", KERNELS)
+@pytest.mark.parametrize("variant", [O.AGGREGATION, O.SOURCES, O.SHATTERING])
+def test_eval_rhs_matches_oracle_small_path(agk, oracle_port, m, kind, alpha, variant):
+    rng = np.random.default_rng(1000 + m)
+    om, ws = make(agk, kind, m, alpha, variant, [(1, 1.0), (min(m, 10), 0.1), (1, 0.5)], 0.01)
+    for _ in range(3):
+        n = rng.random(m)
+        want = oracle_port.eval_rhs(om, n)
+        got = agk.eval_rhs(ws, n)
+        assert rel_max_diff(got, want) <= TOL
+
+
+@pytest.mark.parametrize("m", [4097, 8192, 10000, 1 << 14, 40000, 1 << 16])
+@pytest.mark.parametrize("kind,alpha", [("constant", 0.0), ("brownian", 0.95), ("brownian2", 0.0)])
+@pytest.mark.parametrize("variant", [O.AGGREGATION, O.SOURCES, O.SHATTERING])
+def test_eval_rhs_matches_oracle_four_step(agk, oracle_port, m, kind, alpha, variant):
+    rng = np.random.default_rng(m)
+    om, ws = make(agk, kind, m, alpha, variant, [(1, 1.0), (100, 0.1)], 0.01)
+    n = rng.random(m) * np.exp(-np.arange(m) / (m / 8))
+    want = oracle_port.eval_rhs(om, n)
+    got = agk.eval_rhs(ws, n)
+    assert rel_max_diff(got, want) <= TOL
+
+
+def test_golden_rhs_fixtures(agk):
+    """Reference outputs committed by tests/golden/make_golden.py (from oracle/_ref)."""
+    g = np.load(os.path.join(GOLDEN, "golden_rhs.npz"))
+    for c in range(int(g["count"][0])):
+        m, var, kidx = (int(x) for x in g[f"c{c}_meta"])
+        kind, alpha = KERNELS[kidx]
+        srcs = [(1, 1.0), (min(m, 10), 0.1)] if var == O.SOURCES else []
+        u, v = factors(kind, m, alpha)
+        ws = agk.RhsWorkspace(agk.Model(u, v, var, srcs, 0.01 if var == O.SHATTERING else 0.0))
+        got = agk.eval_rhs(ws, g[f"c{c}_n"])
+        assert rel_max_diff(got, g[f"c{c}_S"]) <= TOL, c
+
+
+def test_hand_values(agk):
+    """test_rhs.cpp:47-143 against the device path."""
+    _, ws = make(agk, "constant", 3)
+    b = agk.birth_term(ws, [1.0, 0.0, 0.0])
+    assert b[0] == 0.0 and abs(b[1] - 0.5) <= 1e-14 and abs(b[2]) <= 1e-14
+    assert np.all(np.abs(agk.birth_term(ws, [0.0, 0.0, 0.0])) <= 1e-15)
+    d = agk.death_term(ws, [1.0, 0.0, 0.0])
+    assert abs(d[0] - 1.0) <= 1e-15 and d[1] == 0.0 and d[2] == 0.0
+    assert np.all(agk.death_term(ws, [0.0, 0.0, 0.0]) == 0.0)
+    s = agk.shattering_terms(ws, [0.0, 1.0, 0.0], 1.0)
+    assert abs(s[0] - 2.0) <= 2e-14 and abs(s[1] + 1.0) <= 1e-14 and s[2] == 0.0
+    assert abs(1.0 * s[0] + 2.0 * s[1] + 3.0 * s[2]) <= 1e-14
+    assert np.all(agk.shattering_terms(ws, np.random.default_rng(3).random(3), 0.0) == 0.0)
+    with pytest.raises(ValueError):
+        agk.shattering_terms(ws, [0.0, 1.0, 0.0], -1.0)
+    out = agk.eval_rhs(ws, [1.0, 0.0, 0.0])
+    assert abs(out[0] + 1.0) <= 1e-14 and abs(out[1] - 0.5) <= 1e-14 and abs(out[2]) <= 1e-14
+    _, ws = make(agk, "constant", 3, variant=O.SOURCES, sources=[(1, 1.0)])
+    out = agk.eval_rhs(ws, [1.0, 0.0, 0.0])
+    assert abs(out[0]) <= 1e-14 and abs(out[1] - 0.5) <= 1e-14
+    _, ws = make(agk, "constant", 3, variant=O.SOURCES, sources=[(2, 0.25)])
+    out = agk.eval_rhs(ws, [0.0, 0.0, 0.0])
+    assert out[0] == 0.0 and out[1] == 0.25 and out[2] == 0.0
+
+
+def birth_truth(u, v, n):
+    """Birth term by direct convolution in long double (x87 80-bit): the accuracy yardstick."""
+    m = n.size
+    x = u.astype(np.longdouble) * n[:, None].astype(np.longdouble)
+    y = v.astype(np.longdouble) * n[None, :].astype(np.longdouble)
+    t = np.zeros(m, dtype=np.longdouble)
+    for a in range(u.shape[1]):
+        t[1:] += 0.5 * np.convolve(x[:, a], y[a])[: m - 1]
+    return t.astype(np.float64)
+
+
+@pytest.mark.parametrize("m", [64, 5000, 12000])
+def test_terms_match_oracle(agk, oracle_port, m):
+    rng = np.random.default_rng(5)
+    om, ws = make(agk, "brownian", m, 0.95, O.SHATTERING, lam=0.01)
+    n = rng.random(m)
+    got, want = agk.birth_term(ws, n), oracle_port.birth_term(om, n)
+    if True:
+        # The packed two-real-FFT trick (rhs.cpp:131-144) mixes U n (~m^0.95) with V n (~m^-0.95):
+        # the reference itself is off the exact birth term by ~6e-11 normwise here, so the device
+        # result is held to the exact value instead: no worse than the reference (or 1e-12).
+        truth = birth_truth(om.u, om.v, n)
+        assert rel_max_diff(got, truth) <= max(1.0 * rel_max_diff(want, truth), 1e-12)
+    assert rel_max_diff(agk.death_term(ws, n), oracle_port.death_term(om, n)) <= TOL
+    assert rel_max_diff(agk.shattering_terms(ws, n, 0.37), oracle_port.shattering_terms(om, n, 0.37)) <= TOL
+    assert agk.birth_term(ws, n)[0] == 0.0  # exact zero (rhs.cpp:147)
+
+
+def test_mass_neutral_shattering(agk):
+    """test_rhs.cpp:98-114."""
+    rng = np.random.default_rng(17)
+    for alpha in (0.0, 0.95):
+        _, ws = make(agk, "brownian", 96, alpha)
+        for _ in range(5):
+            out = agk.shattering_terms(ws, rng.random(96), 0.01)
+            flux = np.dot(np.arange(1, 97), out)
+            assert abs(flux) <= 1e-12 * abs(out[0])
+
+
+def test_truncation_leak_identity(agk):
+    """test_rhs.cpp:215-240: mass flux of the aggregation RHS equals the truncation leak."""
+    rng = np.random.default_rng(37)
+    m = 64
+    u, v = factors("brownian", m, 0.95)
+    ws = agk.RhsWorkspace(agk.Model(u, v))
+    K = u @ v
+    for _ in range(5):
+        n = rng.random(m)
+        out = agk.eval_rhs(ws, n)
+        flux = np.dot(np.arange(1, m + 1), out)
+        leak = 0.0
+        for i in range(1, m + 1):
+            for j in range(m + 1 - i, m + 1):
+                leak += (i + j) * K[i - 1, j - 1] * n[i - 1] * n[j - 1]
+        leak *= -0.5
+        assert abs(flux - leak) <= 1e-12 * abs(leak)
+
+
+def test_bilinearity(agk):
+    """test_rhs.cpp:242-263."""
+    m = 32
+    _, ws = make(agk, "brownian", m, 0.3)
+    n = np.random.default_rng(41).random(m)
+    c = 3.25
+    np.testing.assert_allclose(agk.birth_term(ws, c * n), c * c * agk.birth_term(ws, n), rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(agk.death_term(ws, c * n), c * c * agk.death_term(ws, n), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("m", [40, 1 << 15])
+def test_determinism_and_counter(agk, m):
+    """test_rhs.cpp:265-282: reuse is transparent (bitwise) and the counter counts exactly."""
+    rng = np.random.default_rng(43)
+    _, ws = make(agk, "constant", m)
+    assert ws.evals() == 0
+    for _ in range(4):
+        n = rng.random(m)
+        a = agk.eval_rhs(ws, n)
+        _, fresh = make(agk, "constant", m)
+        b = agk.eval_rhs(fresh, n)
+        assert np.array_equal(a, b)
+    assert ws.evals() == 4
+    ws.reset_evals()
+    assert ws.evals() == 0
+
+
+def test_size_errors(agk):
+    _, ws = make(agk, "constant", 8)
+    with pytest.raises(ValueError):
+        agk.eval_rhs(ws, np.zeros(7))
+    with pytest.raises(ValueError):
+        agk.RhsWorkspace(agk.Model(np.ones((1, 1)), np.ones((1, 1))))  # m < 2
+    with pytest.raises(ValueError):
+        agk.RhsWorkspace(agk.Model(np.ones((8, 1)), np.ones((1, 8)), O.SOURCES, [(9, 1.0)]))
+    with pytest.raises(ValueError):
+        agk.RhsWorkspace(agk.Model(np.ones((8, 1)), np.ones((1, 8)), O.SHATTERING, [], -1.0))
+
+
+def test_euler_bound(agk, oracle_port):
+    """test_rhs.cpp:300-320."""
+    om, ws = make(agk, "constant", 8)
+    n = np.zeros(8)
+    n[0], n[4] = 1.5, 0.5
+    assert abs(agk.euler_stability_bound(ws, n, 0.25) - 0.125) <= 1e-15
+    n = np.zeros(8)
+    n[0] = 1.0
+    assert abs(agk.euler_stability_bound(ws, n, 1.0) - 1.0) <= 1e-15
+    assert math.isinf(agk.euler_stability_bound(ws, np.zeros(8), 0.25))
+    with pytest.raises(ValueError):
+        agk.euler_stability_bound(ws, n, 0.0)
+    om, ws = make(agk, "brownian2", 3000)
+    n = np.random.default_rng(1).random(3000)
+    a = agk.euler_stability_bound(ws, n, 0.25)
+    b = oracle_port.euler_stability_bound(om, n, 0.25)
+    assert abs(a - b) <= 1e-13 * b
+
+
+def test_dedupe_weights(agk, oracle_port):
+    """Ranks folded by the reference's bitwise rule (rhs.cpp:96-124)."""
+    _, ws = make(agk, "brownian", 64, 0.5)
+    assert ws.unique_ranks() == 1
+    _, ws = make(agk, "brownian2", 64)
+    assert ws.unique_ranks() == 2
+    rng = np.random.default_rng(7)
+    m, r = 5000, 6
+    i = np.arange(1, m + 1.0)
+    p = rng.uniform(-0.5, 0.5, r)
+    u = rng.uniform(0.5, 1.5, r)[None, :] * i[:, None] ** p[None, :]
+    v = rng.uniform(0.5, 1.5, r)[:, None] * i[None, :] ** (-p[:, None])
+    u[:, 3], v[3] = u[:, 1], v[1]
+    u[:, 5], v[5] = v[0], u[:, 0]
+    om = O.Model(u, v, O.SHATTERING, [], 0.02)
+    ws = agk.RhsWorkspace(agk.Model(u, v, O.SHATTERING, [], 0.02))
+    assert ws.unique_ranks() == 4
+    n = np.exp(-i / 500.0) * rng.uniform(0.9, 1.1, m)
+    assert rel_max_diff(agk.eval_rhs(ws, n), oracle_port.eval_rhs(om, n)) <= TOL
+
+
+def test_device_pointers(agk, oracle_port):
+    import torch
+    om, ws = make(agk, "brownian2", 20000, variant=O.SOURCES, sources=[(1, 1.0)])
+    n = np.random.default_rng(2).random(20000)
+    got = agk.eval_rhs(ws, torch.from_numpy(n).cuda()).cpu().numpy()
+    assert rel_max_diff(got, oracle_port.eval_rhs(om, n)) <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("variant", [O.AGGREGATION, O.SHATTERING])
+def test_config4_full_shape(agk, oracle_port, variant):
+    """BASELINE config 4 at full size (M=2^20, R=16): one RHS against the oracle."""
+    U, V, n = config4_inputs()
+    om = O.Model(U, V, variant, [], 0.01)
+    ws = agk.RhsWorkspace(agk.Model(U, V, variant, [], 0.01))
+    assert ws.unique_ranks() == 16
+    got = agk.eval_rhs(ws, n)
+    want = oracle_port.eval_rhs(om, n)
+    assert rel_max_diff(got, want) <= TOL
+    # exact zeros where the reference has them: death/shattering loss where n_s == 0
+    zero = n == 0.0
+    assert zero.sum() > 0
+    d = agk.death_term(ws, n)
+    assert np.all(d[zero] == 0.0)
