@@ -1,0 +1,362 @@
+#!/usr/bin/env python3
+"""bench.py — RHS evaluations/s of the low-rank Smoluchowski operator on B200 (BASELINE config 4).
+
+Workload (BASELINE.json configs[3], the configuration the headline metric is quoted on):
+random positive low-rank kernel, R = 16, M = 2^20, fp64, seeded synthetic inputs
+(paper_2407_16559_b200/configs.py). One "step" = one eval_rhs over the state vector.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+* value: K evaluations per rank on device-resident inputs, device time from CUDA events on the
+  handle's stream around the captured per-RHS graph (max over ranks); U/V (256 MiB) exceed the
+  126 MB L2, so every evaluation streams them from HBM (no flush needed).
+* e2e: the same metric through the public C ABI (agk_rhs_eval) with pinned HOST buffers: the
+  H2D copy of n and the D2H copy of S(n) are inside the timed region every step.
+* roofline: the dominant kernel's algorithmic bytes per launch / its event-timed duration.
+* cpu_baseline: the reference compiled from its own sources (oracle/_ref), single thread, on a
+  bounded sample (2 evaluations) on rank 0.
+* --impl reference: the reference's CPU implementation on all host cores (one independent
+  evaluation per thread, as the reference's own bench runs cells on std::threads).
+* N > 1: replicas only (the path does not shard): one independent workload per GPU,
+  no data-path collective; torch.distributed is used only for the barrier and max-over-ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RHS evals/s + HBM GB/s (M=2^20,R=16,fp64); adaptive solve time to t_end"
+UNIT = "RHS evals/s"
+M, R = 1 << 20, 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget-s", type=float, default=240.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ distributed plumbing
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, local):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic counts
+
+def survey_bytes(m, r, rf):
+    """SURVEY §8d two-pass model bytes_alg = M (88 + 16R + 72R_f) and the compulsory 8M(2R+2)."""
+    return m * (88 + 16 * r + 72 * rf), 8 * m * (2 * r + 2)
+
+
+def survey_flops(m, rf):
+    p = 1
+    while p < 2 * m:
+        p *= 2
+    lg = p.bit_length() - 1
+    return 5 * p * lg * (rf + 0.5) + 18 * p * rf
+
+
+def kernel_counts(cls, m, r, rf, plan, first, g):
+    """Algorithmic HBM bytes and fp64 flops of ONE launch of a four-step kernel."""
+    log2p, n1, n2, gs = plan
+    p = 1 << log2p
+    l1, l2 = n1.bit_length() - 1, n2.bit_length() - 1
+    if cls == "col_fwd":
+        return 8 * m + 16 * m * g + 16 * p * g, g * (5 * p * l1 + 6 * p)
+    if cls == "row":
+        return 16 * p * g + 8 * p * (0 if first else 1) + 8 * p, g * (5 * p * l2 + 9 * p) + 5 * (p // 2) * l2
+    if cls == "col_inv":
+        return 8 * p + 8 * m + 8 * m * r + 8 * m, 5 * (p // 2) * l1 + 4 * m * r
+    return 8 * m * (2 * r + 2), survey_flops(m, rf)
+
+
+def load_ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ arms
+
+def cpu_baseline_sample(U, V, n, evals=2):
+    from oracle.oracle import Model, Oracle
+    try:
+        o, kind = Oracle("reference"), "reference"
+    except FileNotFoundError:
+        o, kind = Oracle("port"), "port"
+    md = Model(U, V)
+    t0 = time.perf_counter()
+    for _ in range(evals):
+        o.eval_rhs(md, n)
+    dt = time.perf_counter() - t0
+    return {"value": evals / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{evals} eval_rhs at M=2^20, R=16 (config 4), single thread, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    """The reference's own CPU eval_rhs (oracle/_ref) on all host threads."""
+    if rank != 0:
+        return None
+    from paper_2407_16559_b200.configs import random_config4
+    from oracle.oracle import Model, Oracle
+    try:
+        o, kind = Oracle("reference"), "reference"
+    except FileNotFoundError:
+        o, kind = Oracle("port"), "port"
+    U, V, n = random_config4(M, R)
+    md = Model(U, V)
+    cores = os.cpu_count() or 1
+
+    def one_round():
+        ths = [threading.Thread(target=o.eval_rhs, args=(md, n)) for _ in range(cores)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return time.perf_counter() - t0
+
+    for _ in range(max(1, min(args.warmup, 1))):
+        one_round()
+    times = []
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
+        times.append(one_round())
+        if time.perf_counter() - t_start > args.ref_budget_s:
+            break
+    total = sum(times)
+    value = cores * len(times) / total
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "steps_timed": len(times), "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4: low-rank RHS M=2^20 R=16 random kernel (seed 0x5eed5eed)",
+                   "m": M, "r": R, "threads": cores},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{cores} concurrent eval_rhs per step (one per host thread), "
+                                   f"{len(times)} step(s) timed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def run_b200(args, world, rank, local):
+    import torch
+    import paper_2407_16559_b200 as agk
+    from paper_2407_16559_b200.configs import random_config4
+
+    torch.cuda.set_device(local)
+    U, V, n = random_config4(M, R)
+    ws = agk.RhsWorkspace(agk.Model(U, V), device=local)
+    rf = ws.unique_ranks()
+    n_dev = torch.from_numpy(n).to(f"cuda:{local}")
+    out_dev = torch.empty_like(n_dev)
+    launches = ws.launches_per_eval()
+
+    agk.eval_rhs_timed(ws, n_dev, out_dev, max(args.warmup, 3))  # warm-up (graph capture inside)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = agk.eval_rhs_timed(ws, n_dev, out_dev, args.steps)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = max_over_ranks(ms, world, local)
+    sec = ms * 1e-3
+    value = world * args.steps / sec
+
+    # end to end through the public API with pinned host buffers
+    h_in = torch.from_numpy(n).pin_memory()
+    h_out = torch.empty(M, dtype=torch.float64).pin_memory()
+    lib = agk.load_library()
+    for _ in range(2):
+        agk._check(lib.agk_rhs_eval(ws.handle, h_in.data_ptr(), h_out.data_ptr(), agk.MEM_HOST), ws.handle)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        agk._check(lib.agk_rhs_eval(ws.handle, h_in.data_ptr(), h_out.data_ptr(), agk.MEM_HOST), ws.handle)
+    e2e_sec = max_over_ranks(time.perf_counter() - t0, world, local)
+    e2e = {"value": world * args.steps / e2e_sec, "unit": UNIT, "h2d_bytes_per_step": 8 * M,
+           "d2h_bytes_per_step": 8 * M}
+
+    # per-kernel roofline of the dominant kernel
+    prof, plan = agk.profile_rhs(ws, n_dev, out_dev, reps=5)
+    by_cls = {}
+    first_row = True
+    g = plan[3]
+    per_launch = []
+    for cls, kms in prof:
+        first = first_row if cls == "row" else True
+        if cls == "row":
+            first_row = False
+        b, f = kernel_counts(cls, M, R, rf, plan, first, g)
+        per_launch.append((cls, kms, b, f))
+        d = by_cls.setdefault(cls, {"ms": 0.0, "bytes": 0, "flops": 0, "launches": 0})
+        d["ms"] += kms
+        d["bytes"] += b
+        d["flops"] += f
+        d["launches"] += 1
+    total_ms = sum(d["ms"] for d in by_cls.values())
+    dom = max(by_cls, key=lambda c: by_cls[c]["ms"])
+    dd = by_cls[dom]
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+        hbm_peak, hbm_src = float(peaks["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except Exception:
+        hbm_peak, hbm_src = 6650.0, "B200_PROFILING.md fallback"
+    fp64_peak = 33.8  # TFLOP/s, DFMA microbenchmark on this pool (profiles/probe_r01.txt)
+    avg_ms = dd["ms"] / dd["launches"]
+    ach_gbs = dd["bytes"] / dd["launches"] / (avg_ms * 1e-3) / 1e9
+    ach_tf = dd["flops"] / dd["launches"] / (avg_ms * 1e-3) / 1e12
+    traffic = load_ncu_traffic().get(dom)
+    b_alg, b_comp = survey_bytes(M, R, rf)
+    per_rhs_s = sec / args.steps * world
+    roofline = {
+        "bound": "hbm", "kernel": dom, "achieved": ach_gbs, "peak": hbm_peak, "unit": "GB/s",
+        "frac": ach_gbs / hbm_peak, "traffic": traffic, "peak_source": hbm_src,
+        "share_of_step": dd["ms"] / total_ms, "avg_launch_ms": avg_ms, "launches_per_step": dd["launches"],
+        "alg_bytes_per_launch": dd["bytes"] / dd["launches"],
+        "fp64": {"achieved_tflops": ach_tf, "peak_tflops": fp64_peak, "frac": ach_tf / fp64_peak,
+                 "alg_flops_per_launch": dd["flops"] / dd["launches"],
+                 "peak_source": "DFMA microbenchmark, profiles/probe_r01.txt"},
+        "per_class_ms": {c: by_cls[c]["ms"] for c in by_cls},
+        "whole_rhs": {"bytes_alg_survey": b_alg, "bytes_compulsory": b_comp, "flops_alg": survey_flops(M, rf),
+                      "gbs_survey_model": b_alg / per_rhs_s / 1e9,
+                      "frac_survey_model": b_alg / per_rhs_s / 1e9 / hbm_peak,
+                      "frac_compulsory": b_comp / per_rhs_s / 1e9 / hbm_peak,
+                      "fp64_frac": survey_flops(M, rf) / per_rhs_s / 1e12 / fp64_peak},
+    }
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config4: low-rank RHS M=2^20 R=16 random kernel (seed 0x5eed5eed)",
+                   "m": M, "r": R, "unique_ranks": rf, "plan": {"log2p": plan[0], "n1": plan[1], "n2": plan[2],
+                                                               "ranks_per_group": plan[3]},
+                   "l2": "inputs (U,V 256 MiB) larger than the 126 MB L2; no flush", "parallelism": f"replicas{world}"},
+        "e2e": e2e, "roofline": roofline, "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline_sample(U, V, n)
+    ws.close()
+    return res
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        res = run_reference(args, world, rank)
+    else:
+        res = run_b200(args, world, rank, local)
+    if rank == 0 and res is not None:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -191,6 +191,13 @@ agk_status agk_rhs_eval_timed(agk_rhs* h, const double* n_dev, double* out_dev, 
 /* Number of kernel launches one eval_rhs issues (for bench.py's gpu_launches). */
 int agk_rhs_launches_per_eval(const agk_rhs* h);
 
+/* Per-launch device time of one eval_rhs, averaged over `reps` evaluations: CUDA events are
+ * recorded on the handle's stream between consecutive kernels. ms[i] and cls[i] (kernel class:
+ * 0 single-CTA, 1 column-forward, 2 row, 3 column-inverse) for i < *n (at most cap). Counts
+ * `reps` evaluations. Also reports the plan: log2 P, N1, N2, ranks per group. */
+agk_status agk_rhs_profile(agk_rhs* h, const double* n_dev, double* out_dev, int reps, double* ms, int* cls,
+                           int cap, int* n, int* plan4);
+
 #ifdef __cplusplus
 }
 #endif

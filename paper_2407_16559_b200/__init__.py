@@ -107,6 +107,8 @@ _SIGS = {
     "agk_describe_status": (C.c_char_p, [C.c_int]),
     "agk_rhs_eval_timed": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_float)]),
     "agk_rhs_launches_per_eval": (C.c_int, [C.c_void_p]),
+    "agk_rhs_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, _dp, C.POINTER(C.c_int), C.c_int,
+                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]),
 }
 
 _lib = None
@@ -461,6 +463,30 @@ def run(ws: RhsWorkspace, cfg: SimulationConfig) -> RunReport:
                      "" if rep.termination == 0 else describe(rep.abort_status), rep.abort_t, rep.abort_tau,
                      rep.final_t, final, snapshots, records, rep.num_records, rep.total_rhs_evals,
                      rep.total_accepted, rep.total_rejects, rep.wall_seconds)
+
+
+KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv")
+
+
+def eval_rhs_timed(ws: RhsWorkspace, n_dev, out_dev, count: int) -> float:
+    """Device milliseconds for `count` back-to-back evaluations on device tensors (CUDA events
+    on the workspace's stream around the captured per-RHS graph)."""
+    ms = C.c_float()
+    _check(load_library().agk_rhs_eval_timed(ws.handle, n_dev.data_ptr(), out_dev.data_ptr(), count, C.byref(ms)),
+           ws.handle)
+    return ms.value
+
+
+def profile_rhs(ws: RhsWorkspace, n_dev, out_dev, reps: int = 5):
+    """Per-launch device times of one evaluation: [(class, ms)], plus (log2P, N1, N2, group)."""
+    cap = 256
+    ms = (C.c_double * cap)()
+    cls = (C.c_int * cap)()
+    nk = C.c_int()
+    plan = (C.c_int * 4)()
+    _check(load_library().agk_rhs_profile(ws.handle, n_dev.data_ptr(), out_dev.data_ptr(), reps, ms, cls, cap,
+                                          C.byref(nk), plan), ws.handle)
+    return [(KERNEL_CLASSES[cls[i]], ms[i]) for i in range(nk.value)], tuple(plan)
 
 
 def moments(n, orders=(0, 1, 2)):

@@ -50,6 +50,8 @@ struct agk_rhs {
   std::map<int, cudaGraphExec_t> graphs;
   std::map<int, int> graph_kernels;
   cudaGraphExec_t rhs_graph = nullptr;
+  const double* rhs_graph_in = nullptr;
+  double* rhs_graph_out = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -814,7 +816,13 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
 agk_status agk_rhs_eval_timed(agk_rhs* h, const double* n_dev, double* out_dev, int count, float* elapsed_ms) {
   if (!h || h->kind != AGK_RHS_MODEL || count < 1) return fail(h, AGK_ERR_INVALID_ARGUMENT, "bad timing request");
   DeviceGuard dg(h->device);
+  if (h->rhs_graph && (h->rhs_graph_in != n_dev || h->rhs_graph_out != out_dev)) {
+    cudaGraphExecDestroy(h->rhs_graph);
+    h->rhs_graph = nullptr;
+  }
   if (!h->rhs_graph) {
+    h->rhs_graph_in = n_dev;
+    h->rhs_graph_out = out_dev;
     cudaGraph_t g;
     RhsArgs a = h->base;
     a.n = VecRef{n_dev, nullptr, 0};
@@ -833,6 +841,40 @@ agk_status agk_rhs_eval_timed(agk_rhs* h, const double* n_dev, double* out_dev, 
   CK_H(h, cudaEventSynchronize(h->ev1), "event sync");
   CK_H(h, cudaEventElapsedTime(elapsed_ms, h->ev0, h->ev1), "elapsed");
   h->evals += (uint64_t)count;
+  return AGK_OK;
+}
+
+agk_status agk_rhs_profile(agk_rhs* h, const double* n_dev, double* out_dev, int reps, double* ms, int* cls, int cap,
+                           int* n, int* plan4) {
+  if (!h || h->kind != AGK_RHS_MODEL || reps < 1 || cap < 1) return fail(h, AGK_ERR_INVALID_ARGUMENT, "bad profile request");
+  DeviceGuard dg(h->device);
+  std::vector<cudaEvent_t> ev(cap + 1);
+  for (auto& e : ev) CK_H(h, cudaEventCreate(&e), "event");
+  std::vector<double> acc(cap, 0.0);
+  int nk = 0;
+  RhsArgs a = h->base;
+  a.n = VecRef{n_dev, nullptr, 0};
+  a.out = out_dev;
+  for (int q = 0; q < reps; ++q) {
+    CK_H(h, cudaEventRecord(ev[0], h->stream), "event");
+    CK_H(h, rhs_launch_marked(h->plan, a, h->stream, ev.data() + 1, cls, cap, &nk), "rhs launch");
+    CK_H(h, cudaStreamSynchronize(h->stream), "sync");
+    for (int k = 0; k < nk; ++k) {
+      float t = 0.f;
+      CK_H(h, cudaEventElapsedTime(&t, ev[k], ev[k + 1]), "elapsed");
+      acc[k] += t;
+    }
+  }
+  for (int k = 0; k < nk; ++k) ms[k] = acc[k] / reps;
+  *n = nk;
+  if (plan4) {
+    plan4[0] = h->plan.log2p;
+    plan4[1] = h->plan.small ? 0 : h->plan.n1;
+    plan4[2] = h->plan.small ? 0 : h->plan.n2;
+    plan4[3] = h->plan.gsize;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  h->evals += (uint64_t)reps;
   return AGK_OK;
 }
 

@@ -133,33 +133,89 @@ __device__ __forceinline__ void dft_halfzero(double2* x) {
 
 __host__ __device__ constexpr int ilog2(int n) { return n <= 1 ? 0 : 1 + ilog2(n / 2); }
 
+// ---- asynchronous global -> shared copies (LDGSTS): next work item's operands are staged
+// while the current item's transforms run. src_bytes = 0 zero-fills (out-of-range elements).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 // Shared-memory index padding: one spare slot every 2^S entries breaks the bank conflicts of
-// the radix-2^S first pass (stride 2^S x 16 B).
+// the radix-2^S first pass (stride 2^S x 16 B). S >= 30 means no padding (the column kernels
+// interleave teams across lanes, which already spreads the banks).
 template <int S>
 __device__ __forceinline__ int pad_idx(int i) {
-  return i + (i >> S);
+  if constexpr (S >= 30) {
+    return i;
+  } else {
+    return i + (i >> S);
+  }
 }
 template <int N, int S>
 struct Padded {
-  static constexpr int value = N + (N >> S) + 1;  // +1: successive team regions start on different banks
+  // +1: successive team regions start on different banks
+  static constexpr int value = (S >= 30 ? N : N + (N >> S)) + 1;
 };
+constexpr int kNoPad = 30;
 
-// Accurate table of W_NT^k = exp(-2*pi*i*k/NT), k < NT, NT a power of two >= N.
+// Accurate table of W_N^k = exp(-2*pi*i*k/N), k < N, in global memory (host long double).
 struct TwTable {
   const double2* w;
   int log2n;
 };
 
-template <int SIGN>
-__device__ __forceinline__ double2 tw_lookup(const TwTable& t, int k) {
-  const double2 w = __ldg(t.w + k);
-  return SIGN < 0 ? w : cconj(w);
+// Pass schedule: first pass radix R0 = 2^(log2N mod log2E) if nonzero (so that the Ns=1 pass,
+// which carries the zero-padding, can be the small one), then NFULL passes of radix E.
+// Inter-pass twiddles live in shared memory, one table per full pass laid out [r-1][k]
+// (k = b mod Ns fastest) so that consecutive lanes read consecutive entries.
+template <int N, int E>
+struct FftPlan {
+  static constexpr int L = ilog2(N), LE = ilog2(E);
+  static constexpr int REM = L % LE;
+  static constexpr int R0 = REM ? (1 << REM) : E;
+  static constexpr int NFULL = REM ? L / LE : L / LE - 1;
+  static constexpr int PADS = ilog2(R0) > 0 ? ilog2(R0) : 1;
+  template <int PS>
+  static constexpr int smem() { return Padded<N, PS>::value; }  // double2 entries per team
+  static constexpr int SMEM = Padded<N, PADS>::value;
+  static constexpr int tw_off(int i) {
+    int off = 0, ns = R0;
+    for (int q = 0; q < i; ++q) {
+      off += (E - 1) * ns;
+      ns *= E;
+    }
+    return off;
+  }
+  static constexpr int TWS = tw_off(NFULL);  // double2 entries of the twiddle tables
+};
+
+// Fill the plan's shared twiddle tables from the global W_N table (cooperative, all threads).
+template <int N, int E>
+__device__ __forceinline__ void load_twiddles(double2* smtw, const TwTable& g) {
+  using P = FftPlan<N, E>;
+  for (int idx = threadIdx.x; idx < P::TWS; idx += blockDim.x) {
+    int off = 0, ns = P::R0, pass = 0;
+    while (idx >= off + (E - 1) * ns) {
+      off += (E - 1) * ns;
+      ns *= E;
+      ++pass;
+    }
+    const int rel = idx - off, r = rel / ns + 1, k = rel % ns;
+    // W_{ns E}^{k r} = W_N^{k r N / (ns E)}
+    smtw[idx] = __ldg(g.w + (int64_t)k * r * (N / (ns * E)));
+  }
 }
 
 // One Stockham pass of radix R over a team's data (see file header for the layout).
 template <int N, int E, int R, int SIGN, int PADS, bool LAST, bool HALFZERO>
 __device__ __forceinline__ void stockham_pass(double2 (&v)[E], double2* sm, int j, int ns,
-                                              const TwTable& tw, bool active) {
+                                              const double2* twp, bool active) {
   constexpr int T = N / E;
   constexpr int Q = E / R;
   if (active) {
@@ -171,10 +227,11 @@ __device__ __forceinline__ void stockham_pass(double2 (&v)[E], double2* sm, int 
 #pragma unroll
       for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
       if (ns > 1) {
-        // W_{ns*R}^{k*r} = W_NT^{k*r*NT/(ns*R)}
-        const int shift = tw.log2n - ilog2(R) - (31 - __clz(ns));
 #pragma unroll
-        for (int r = 1; r < R; ++r) u[r] = cmul(u[r], tw_lookup<SIGN>(tw, (k * r) << shift));
+        for (int r = 1; r < R; ++r) {
+          const double2 w = twp[(r - 1) * ns + k];
+          u[r] = cmul(u[r], SIGN < 0 ? w : cconj(w));
+        }
       }
       if constexpr (HALFZERO) {
         dft_halfzero<R, SIGN>(u);
@@ -201,34 +258,24 @@ __device__ __forceinline__ void stockham_pass(double2 (&v)[E], double2* sm, int 
   }
 }
 
-// Pass schedule: first pass radix = 2^(log2N mod log2E) if nonzero (so that the Ns=1 pass,
-// which carries the zero-padding, can be the small one), then passes of radix E.
-template <int N, int E>
-struct FftPlan {
-  static constexpr int L = ilog2(N), LE = ilog2(E);
-  static constexpr int REM = L % LE;
-  static constexpr int R0 = REM ? (1 << REM) : E;  // radix of the first (Ns = 1) pass
-  static constexpr int NFULL = REM ? L / LE : L / LE - 1;  // radix-E passes after the first
-  static constexpr int PADS = ilog2(R0) > 0 ? ilog2(R0) : 1;
-  static constexpr int SMEM = Padded<N, PADS>::value;  // double2 entries per team
-};
-
 template <int N, int E, int SIGN, int PADS, int IDX, int NPASS>
 struct FullPasses {
   __device__ __forceinline__ static void run(double2 (&v)[E], double2* sm, int j, int ns,
-                                             const TwTable& tw, bool active) {
+                                             const double2* smtw, bool active) {
     if constexpr (IDX < NPASS) {
-      stockham_pass<N, E, E, SIGN, PADS, IDX == NPASS - 1, false>(v, sm, j, ns, tw, active);
-      FullPasses<N, E, SIGN, PADS, IDX + 1, NPASS>::run(v, sm, j, ns * E, tw, active);
+      stockham_pass<N, E, E, SIGN, PADS, IDX == NPASS - 1, false>(
+          v, sm, j, ns, smtw + FftPlan<N, E>::tw_off(IDX), active);
+      FullPasses<N, E, SIGN, PADS, IDX + 1, NPASS>::run(v, sm, j, ns * E, smtw, active);
     }
   }
 };
 
-// N-point FFT by a team of N/E threads (team-local smem region `sm`, FftPlan::SMEM entries).
-// Every thread of the CTA must call it (barriers); inactive threads pass active=false.
+// N-point FFT by a team of N/E threads (team-local smem region `sm`, FftPlan::smem<PADS>()
+// entries; shared twiddle tables `smtw` filled by load_twiddles<N,E>). Every thread of the CTA
+// must call it (barriers); inactive threads pass active=false.
 // HALFZERO: entries x[N/2..N) are zero on entry (v[r] for r >= E/2 are ignored).
-template <int N, int E, int SIGN, bool HALFZERO>
-__device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, const TwTable& tw,
+template <int N, int E, int SIGN, bool HALFZERO, int PADS = FftPlan<N, E>::PADS>
+__device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, const double2* smtw,
                                           bool active = true) {
   using P = FftPlan<N, E>;
   static_assert(E <= N, "E must not exceed N");
@@ -236,8 +283,8 @@ __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, c
     return;
   } else {
     constexpr bool only = (P::NFULL == 0);
-    stockham_pass<N, E, P::R0, SIGN, P::PADS, only, HALFZERO>(v, sm, j, 1, tw, active);
-    FullPasses<N, E, SIGN, P::PADS, 0, P::NFULL>::run(v, sm, j, P::R0, tw, active);
+    stockham_pass<N, E, P::R0, SIGN, PADS, only, HALFZERO>(v, sm, j, 1, nullptr, active);
+    FullPasses<N, E, SIGN, PADS, 0, P::NFULL>::run(v, sm, j, P::R0, smtw, active);
   }
 }
 

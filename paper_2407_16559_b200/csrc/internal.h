@@ -72,9 +72,15 @@ struct RhsPlan {
   int launches;  // kernels per RHS
 };
 
+// kernel classes for per-launch timing
+enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3 };
+
 // host-side launchers (rhs.cu)
 void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);
 cudaError_t rhs_launch(const RhsPlan& plan, const RhsArgs& a, cudaStream_t s);
+// same, recording ev[i] after the i-th kernel (class cls[i]); *n = kernels launched
+cudaError_t rhs_launch_marked(const RhsPlan& plan, const RhsArgs& a, cudaStream_t s, cudaEvent_t* ev, int* cls,
+                              int cap, int* n);
 size_t rhs_y_elems(const RhsPlan& plan);
 size_t rhs_acc_elems(const RhsPlan& plan);
 size_t rhs_partial_elems(const RhsPlan& plan, int rf);

@@ -94,7 +94,7 @@ __device__ __forceinline__ double epilogue(const RhsArgs& a, const double* __res
   double res = (a.flags & T_BIRTH) ? birth : 0.0;
   if (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) {
     double rowsum = 0.0;
-    for (int ra = 0; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + jo) * __ldg(a.scalars + ra);
+    for (int ra = 0; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + jo) * a.scalars[ra];
     const double nn = n[jo];
     if (a.flags & T_DEATH) res = res - nn * rowsum;
     if (a.flags & T_DEATH_POS) res = nn * rowsum;
@@ -145,18 +145,23 @@ struct SmallCfg {
   static constexpr int E = P >= 16 ? 16 : P;
   static constexpr int T = P / E;
   static constexpr int NT = T < 128 ? 128 : T;
+  using PL = FftPlan<P, E>;
+  static constexpr size_t SMEM_BYTES = (size_t)(PL::SMEM + PL::TWS) * sizeof(double2);
+  static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
 template <int P>
 __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
   using CF = SmallCfg<P>;
   constexpr int E = CF::E, T = CF::T, NT = CF::NT;
-  using PL = FftPlan<P, E>;
+  using PL = typename CF::PL;
   constexpr int H = P / 2 + 1;
   constexpr int QA = (H + NT - 1) / NT;
   extern __shared__ double2 zs[];
+  double2* smtw = zs + PL::SMEM;
   __shared__ double red[(NT / 32) * 4];
   if (a.skip && *a.skip) return;
+  load_twiddles<P, E>(smtw, a.tw_small);
   const int tid = threadIdx.x;
   const int64_t m = a.m;
   const double* __restrict__ n = a.n.get();
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
       for (int r = 0; r < E; ++r) v[r] = zs[pad_idx<PL::PADS>(tid + r * T)];
     }
     __syncthreads();
-    block_fft<P, E, -1, false>(v, zs, tid, a.tw_small, act);
+    block_fft<P, E, -1, false>(v, zs, tid, smtw, act);
     if (act) {
 #pragma unroll
       for (int r = 0; r < E; ++r) zs[pad_idx<PL::PADS>(tid + r * T)] = v[r];
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
     for (int r = 0; r < E; ++r) v[r] = zs[pad_idx<PL::PADS>(tid + r * T)];
   }
   __syncthreads();
-  block_fft<P, E, +1, false>(v, zs, tid, a.tw_small, act);
+  block_fft<P, E, +1, false>(v, zs, tid, smtw, act);
   if (act) {
 #pragma unroll
     for (int r = 0; r < E; ++r) zs[pad_idx<PL::PADS>(tid + r * T)] = v[r];
@@ -249,65 +254,107 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
 
 // ------------------------------------------------------------------ four-step path
 
-template <int L>
+template <int L, int E1_ = ((1 << (L / 2)) >= 256 ? 16 : 8), int E2_ = ((1 << (L - L / 2)) >= 256 ? 16 : 8),
+          int C_ = (L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2))))>
 struct Cfg {
   static constexpr int N1 = 1 << (L / 2), N2 = 1 << (L - L / 2);
-  static constexpr int E1 = N1 >= 256 ? 16 : 8;
-  static constexpr int E2 = N2 >= 256 ? 16 : 8;
-  static constexpr int C = L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 4));
+  static constexpr int E1 = E1_;
+  static constexpr int E2 = E2_;
+  static constexpr int C = C_;
   static constexpr int CP = C / 2 > 0 ? C / 2 : 1;
   static constexpr int T1 = N1 / E1, T2 = N2 / E2;
+  using PL1 = FftPlan<N1, E1>;
+  using PL2 = FftPlan<N2, E2>;
+  static constexpr int R1 = PL1::template smem<kNoPad>();  // column team region (no padding)
+  // + staging of the next rank's U, V (column kernel) / Y rows (row kernel)
+  static constexpr size_t SM_COLFWD = (size_t)(C * R1 + PL1::TWS) * sizeof(double2) + (size_t)C * N1 * sizeof(double);
+  static constexpr bool ROW_STAGE = (2 * PL2::SMEM + PL2::TWS + 2 * N2) * 16 <= 232448;
+  static constexpr size_t SM_ROW = (size_t)(2 * PL2::SMEM + PL2::TWS + (ROW_STAGE ? 2 * N2 : 0)) * sizeof(double2);
+  static constexpr size_t SM_COLINV = (size_t)(CP * R1 + PL1::TWS) * sizeof(double2);
+  static_assert(SM_COLFWD <= 232448 && SM_ROW <= 232448 && SM_COLINV <= 232448, "shared memory budget");
+  static_assert(C * T1 >= 32 && 2 * T2 >= 32, "column-forward and row CTAs need full warps");
+};
+
+// Four-step twiddles W_P^{SIGN e} for e = e0 + r*de, r = 0..E-1, by a short recurrence from two
+// accurate two-level lookups (error ~r ulp, no per-element table loads).
+template <int SIGN>
+struct TwSeries {
+  double2 w, st;
+  __device__ __forceinline__ TwSeries(const TwoLevel& t, uint32_t e0, uint32_t de)
+      : w(tw_p<SIGN>(t, e0)), st(tw_p<SIGN>(t, de)) {}
+  __device__ __forceinline__ double2 next() {
+    const double2 cur = w;
+    w = cmul(w, st);
+    return cur;
+  }
 };
 
 template <int N1, int E1, int C>
 __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int gcount) {
   using PL = FftPlan<N1, E1>;
-  constexpr int T1 = N1 / E1;
+  constexpr int T1 = N1 / E1, NT = C * T1, H = E1 / 2;
+  constexpr int RG = PL::template smem<kNoPad>();
   extern __shared__ double2 smem[];
-  __shared__ double red[((C * T1 + 31) / 32) * 4];
+  double2* smtw = smem + C * RG;
+  double* stage = reinterpret_cast<double*>(smtw + PL::TWS);  // [2][H][NT]: own elements only
+  __shared__ double red[((NT + 31) / 32) * 4];
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, c = tid % C, j = tid / C;
   const int64_t n2 = (int64_t)blockIdx.x * C + c;
   const int64_t N2 = a.n2, m = a.m, P = (int64_t)N1 * N2;
-  const double* __restrict__ n = a.n.get();
-  double nl[E1 / 2];
+  // stage this thread's U_a, V_a elements of unique rank ub (zero-filled past m)
+  auto prefetch = [&](int ub) {
+    const int ra = a.uniq_rank[ub];
+    const double* ut = a.ut + (int64_t)ra * m;
+    const double* vv = a.v + (int64_t)ra * m;
 #pragma unroll
-  for (int r = 0; r < E1 / 2; ++r) {
+    for (int r = 0; r < H; ++r) {
+      const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
+      const bool ok = i < m;
+      cp_async8(stage + r * NT + tid, ut + (ok ? i : 0), ok);
+      cp_async8(stage + (H + r) * NT + tid, vv + (ok ? i : 0), ok);
+    }
+    cp_async_commit();
+  };
+  if (gcount > 0) prefetch(g0);
+  load_twiddles<N1, E1>(smtw, a.tw_n1);
+  const double* __restrict__ n = a.n.get();
+  double nl[H];
+#pragma unroll
+  for (int r = 0; r < H; ++r) {
     const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
     nl[r] = i < m ? n[i] : 0.0;
   }
-  double2* sm = smem + c * PL::SMEM;
+  double2* sm = smem + c * RG;
   for (int g = 0; g < gcount; ++g) {
     const int ub = g0 + g;
-    const int ra = a.uniq_rank[ub];
-    const double* __restrict__ ut = a.ut + (int64_t)ra * m;
-    const double* __restrict__ vv = a.v + (int64_t)ra * m;
     double s[4] = {0.0, 0.0, 0.0, 0.0};
     double2 v[E1];
+    cp_async_wait_all();
 #pragma unroll
-    for (int r = 0; r < E1 / 2; ++r) {
+    for (int r = 0; r < H; ++r) {
       const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
-      v[r] = czero();
-      if (i < m) {
-        const double x = __ldg(ut + i) * nl[r], y = __ldg(vv + i) * nl[r];
-        v[r] = make_double2(x, y);
-        if (i >= 1) {
-          const double sz = (double)(i + 1);
-          s[0] += x;
-          s[1] += sz * x;
-          s[2] += y;
-          s[3] += sz * y;
-        }
+      const double x = stage[r * NT + tid] * nl[r], y = stage[(H + r) * NT + tid] * nl[r];
+      v[r] = make_double2(x, y);
+      if (i >= 1) {  // zero-filled past m: contributes nothing
+        const double sz = (double)(i + 1);
+        s[0] += x;
+        s[1] += sz * x;
+        s[2] += y;
+        s[3] += sz * y;
       }
     }
+    if (g + 1 < gcount) prefetch(ub + 1);  // overlaps this rank's transforms
 #pragma unroll
-    for (int r = E1 / 2; r < E1; ++r) v[r] = czero();
-    block_fft<N1, E1, -1, true>(v, sm, j, a.tw_n1);
+    for (int r = H; r < E1; ++r) v[r] = czero();
+    __syncthreads();  // twiddle tables ready / previous rank's smem reads done
+    block_fft<N1, E1, -1, true, kNoPad>(v, sm, j, smtw);
     double2* __restrict__ yg = a.y + (int64_t)g * P;
+    TwSeries<-1> tw(a.twp, (uint32_t)(n2 * j), (uint32_t)(n2 * T1));
 #pragma unroll
     for (int r = 0; r < E1; ++r) {
       const int64_t k1 = j + r * T1;
-      yg[k1 * N2 + n2] = cmul(v[r], tw_p<-1>(a.twp, (uint32_t)(n2 * k1)));
+      yg[k1 * N2 + n2] = cmul(v[r], tw.next());
     }
     block_sum<4>(s, red);
     if (tid == 0) {
@@ -317,18 +364,29 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   }
 }
 
-template <int N2, int E2>
+template <int N2, int E2, bool STAGE>
 __global__ void __launch_bounds__(2 * (N2 / E2)) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
   using PL = FftPlan<N2, E2>;
   constexpr int T2 = N2 / E2, NT = 2 * T2, Q = E2 / 2;
-  using PLI = FftPlan<N2, Q>;
   extern __shared__ double2 smem[];
+  double2* smtw = smem + 2 * PL::SMEM;
+  double2* stage = smtw + PL::TWS;  // [E2][NT]: this thread's elements of the next rank's row
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, team = tid / T2, j = tid % T2;
   const int n1 = a.n1;
   const int k1 = blockIdx.x;
   const int row = team == 0 ? k1 : (n1 - k1) & (n1 - 1);
   const int64_t P = (int64_t)n1 * N2;
+  auto prefetch = [&](int g) {
+    if constexpr (STAGE) {
+      const double2* yr = a.y + (int64_t)g * P + (int64_t)row * N2;
+#pragma unroll
+      for (int r = 0; r < E2; ++r) cp_async16(stage + r * NT + tid, yr + j + r * T2);
+      cp_async_commit();
+    }
+  };
+  if (gcount > 0) prefetch(0);
+  load_twiddles<N2, E2>(smtw, a.tw_n2);
 
   if (last && blockIdx.x == 0) {
     double* tot = a.scalars + a.r + 2;
@@ -344,11 +402,19 @@ __global__ void __launch_bounds__(2 * (N2 / E2)) k_row(RhsArgs a, int g0, int gc
   double2* smt = smem + team * PL::SMEM;
   for (int g = 0; g < gcount; ++g) {
     const double wt = a.uniq_weight[g0 + g];
-    const double2* __restrict__ yr = a.y + (int64_t)g * P + (int64_t)row * N2;
     double2 v[E2];
+    if constexpr (STAGE) {
+      cp_async_wait_all();
 #pragma unroll
-    for (int r = 0; r < E2; ++r) v[r] = yr[j + r * T2];
-    block_fft<N2, E2, -1, false>(v, smt, j, a.tw_n2);
+      for (int r = 0; r < E2; ++r) v[r] = stage[r * NT + tid];
+      if (g + 1 < gcount) prefetch(g + 1);
+    } else {
+      const double2* __restrict__ yr = a.y + (int64_t)g * P + (int64_t)row * N2;
+#pragma unroll
+      for (int r = 0; r < E2; ++r) v[r] = yr[j + r * T2];
+    }
+    __syncthreads();  // twiddle tables ready / previous rank's split reads done
+    block_fft<N2, E2, -1, false>(v, smt, j, smtw);
 #pragma unroll
     for (int r = 0; r < E2; ++r) smt[pad_idx<PL::PADS>(j + r * T2)] = v[r];
     __syncthreads();
@@ -362,26 +428,32 @@ __global__ void __launch_bounds__(2 * (N2 / E2)) k_row(RhsArgs a, int g0, int gc
       acc[q].x += wt * pr.x;
       acc[q].y += wt * pr.y;
     }
-    __syncthreads();
   }
   if (!last) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) a.acc[(int64_t)k1 * N2 + tid + q * NT] = acc[q];
     return;
   }
-  // inverse row transform of the Hermitian half-row k1, then the inverse four-step twiddle
-#pragma unroll
-  for (int q = 0; q < Q; ++q) smem[pad_idx<PLI::PADS>(tid + q * NT)] = acc[q];
+  // inverse row transform of the Hermitian half-row k1 (team 0), then the inverse twiddle
   __syncthreads();
-  double2 u[Q];
 #pragma unroll
-  for (int r = 0; r < Q; ++r) u[r] = smem[pad_idx<PLI::PADS>(tid + r * NT)];
+  for (int q = 0; q < Q; ++q) smem[pad_idx<PL::PADS>(tid + q * NT)] = acc[q];
   __syncthreads();
-  block_fft<N2, Q, +1, false>(u, smem, tid, a.tw_n2);
+  double2 u[E2];
+  const bool act = team == 0;
+  if (act) {
 #pragma unroll
-  for (int r = 0; r < Q; ++r) {
-    const int64_t c2 = tid + r * NT;
-    a.acc[(int64_t)k1 * N2 + c2] = cmul(u[r], tw_p<+1>(a.twp, (uint32_t)(c2 * k1)));
+    for (int r = 0; r < E2; ++r) u[r] = smem[pad_idx<PL::PADS>(j + r * T2)];
+  }
+  __syncthreads();
+  block_fft<N2, E2, +1, false>(u, smem, j, smtw, act);
+  if (act) {
+    TwSeries<+1> tw(a.twp, (uint32_t)(j * k1), (uint32_t)(T2 * k1));
+#pragma unroll
+    for (int r = 0; r < E2; ++r) {
+      const int64_t c2 = j + r * T2;
+      a.acc[(int64_t)k1 * N2 + c2] = cmul(u[r], tw.next());
+    }
   }
 }
 
@@ -389,8 +461,11 @@ template <int N1, int E1, int CP>
 __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
   using PL = FftPlan<N1, E1>;
   constexpr int T1 = N1 / E1;
+  constexpr int RG = PL::template smem<kNoPad>();
   extern __shared__ double2 smem[];
+  double2* smtw = smem + CP * RG;
   if (a.skip && *a.skip) return;
+  load_twiddles<N1, E1>(smtw, a.tw_n1);
   const int tid = threadIdx.x, c = tid % CP, j = tid / CP;
   const int64_t N2 = a.n2, m = a.m;
   const int64_t col = (int64_t)blockIdx.x * 2 * CP + 2 * c;
@@ -408,7 +483,8 @@ __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
     }
     v[r] = make_double2(ga.x - gb.y, ga.y + gb.x);  // G_a + i G_b: two real outputs at once
   }
-  block_fft<N1, E1, +1, false>(v, smem + c * PL::SMEM, j, a.tw_n1);
+  __syncthreads();
+  block_fft<N1, E1, +1, false, kNoPad>(v, smem + c * RG, j, smtw);
   const double* __restrict__ n = a.n.get();
   const double scale = ldexp(0.5, -a.log2p);
 #pragma unroll
@@ -459,14 +535,16 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   int64_t P = 1;
   while (P < 2 * m) P <<= 1;
   p->log2p = ilog2_host(P);
-  p->small = P <= 8192;
+  p->small = P <= 4096;
   p->n1 = 1 << (p->log2p / 2);
   p->n2 = 1 << (p->log2p - p->log2p / 2);
   const int L = p->log2p;
-  p->c = L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 4));
+  p->c = L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2)));
   p->cp = p->c / 2 > 0 ? p->c / 2 : 1;
-  // Ranks per group: keep the group intermediate (16 B x P per rank) well inside the 126 MB L2.
-  int g = (int)((48ll << 20) / (16 * P));
+  // Ranks per group: all unique ranks in one column/row launch pair (measured fastest at
+  // M = 2^20, R = 16: the per-group intermediate then streams through HBM, but the launches and
+  // the accumulator round trips of smaller groups cost more), capped at 1 GiB of intermediate.
+  int g = (int)((1ll << 30) / (16 * P));
   if (const char* env = getenv("AGK_RANK_GROUP")) g = atoi(env);
   if (g < 1) g = 1;
   if (g > rf) g = rf;
@@ -478,89 +556,151 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
 size_t rhs_acc_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)(p.n1 / 2 + 1) * p.n2; }
 size_t rhs_partial_elems(const RhsPlan& p, int rf) {
-  const size_t nblk = p.small ? 1 : (size_t)(p.n2 / p.c);
+  const size_t nblk = p.small ? 1 : (size_t)(p.n2 / 2);  // enough for any column-block width >= 2
   return (size_t)rf * nblk * 4;
 }
 
+// Optional per-launch event markers (bench.py's per-kernel roofline): after each kernel the
+// launcher records marks->ev[marks->n++] and tags it with the kernel class.
+struct Marks {
+  cudaEvent_t* ev;
+  int* cls;
+  int cap, n;
+};
+static void mark(Marks* mk, int cls, cudaStream_t s) {
+  if (mk && mk->n < mk->cap) {
+    cudaEventRecord(mk->ev[mk->n], s);
+    mk->cls[mk->n++] = cls;
+  }
+}
+
 template <int P>
-static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s) {
-  using PL = FftPlan<P, SmallCfg<P>::E>;
-  k_small<P><<<1, SmallCfg<P>::NT, PL::SMEM * sizeof(double2), s>>>(a);
+static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s, Marks* mk) {
+  k_small<P><<<1, SmallCfg<P>::NT, SmallCfg<P>::SMEM_BYTES, s>>>(a);
+  mark(mk, K_SMALL, s);
   return cudaGetLastError();
 }
 
-template <int L>
-static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s) {
-  using CF = Cfg<L>;
+template <typename CF>
+static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, Marks* mk) {
   RhsArgs a = a0;
   a.nblk_colfwd = CF::N2 / CF::C;
-  const size_t sm1 = (size_t)CF::C * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2);
-  const size_t sm2 = (size_t)2 * FftPlan<CF::N2, CF::E2>::SMEM * sizeof(double2);
-  const size_t sm3 = (size_t)CF::CP * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2);
+  const size_t sm1 = CF::SM_COLFWD, sm2 = CF::SM_ROW, sm3 = CF::SM_COLINV;
   for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     k_col_fwd<CF::N1, CF::E1, CF::C><<<CF::N2 / CF::C, CF::C * CF::T1, sm1, s>>>(a, g0, gc);
-    k_row<CF::N2, CF::E2><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
+    mark(mk, K_COL_FWD, s);
+    k_row<CF::N2, CF::E2, CF::ROW_STAGE><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
+    mark(mk, K_ROW, s);
   }
   k_col_inv<CF::N1, CF::E1, CF::CP><<<CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s>>>(a);
+  mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }
 
-cudaError_t rhs_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s) {
+// Tuning variants of the M = 2^20 shape (AGK_VARIANT), default 0.
+#define AGK_L21_VARIANTS(X) \
+  X(0, 16, 16, 8) X(1, 16, 16, 4) X(2, 8, 16, 8) X(3, 8, 8, 8) X(4, 8, 8, 4) X(5, 16, 8, 4)
+
+static int l21_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AGK_VARIANT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int L>
+static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
+  if constexpr (L == 21) {
+    switch (l21_variant()) {
+#define AGK_X(id, e1, e2, c) \
+  case id: return launch_four_step_cf<Cfg<21, e1, e2, c>>(p, a, s, mk);
+      AGK_L21_VARIANTS(AGK_X)
+#undef AGK_X
+      default: break;
+    }
+  }
+  return launch_four_step_cf<Cfg<L>>(p, a, s, mk);
+}
+
+static cudaError_t rhs_launch_impl(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
   switch (p.log2p) {
-    case 2: return launch_small<4>(a, s);
-    case 3: return launch_small<8>(a, s);
-    case 4: return launch_small<16>(a, s);
-    case 5: return launch_small<32>(a, s);
-    case 6: return launch_small<64>(a, s);
-    case 7: return launch_small<128>(a, s);
-    case 8: return launch_small<256>(a, s);
-    case 9: return launch_small<512>(a, s);
-    case 10: return launch_small<1024>(a, s);
-    case 11: return launch_small<2048>(a, s);
-    case 12: return launch_small<4096>(a, s);
-    case 13: return launch_small<8192>(a, s);
-    case 14: return launch_four_step<14>(p, a, s);
-    case 15: return launch_four_step<15>(p, a, s);
-    case 16: return launch_four_step<16>(p, a, s);
-    case 17: return launch_four_step<17>(p, a, s);
-    case 18: return launch_four_step<18>(p, a, s);
-    case 19: return launch_four_step<19>(p, a, s);
-    case 20: return launch_four_step<20>(p, a, s);
-    case 21: return launch_four_step<21>(p, a, s);
-    case 22: return launch_four_step<22>(p, a, s);
-    case 23: return launch_four_step<23>(p, a, s);
+    case 2: return launch_small<4>(a, s, mk);
+    case 3: return launch_small<8>(a, s, mk);
+    case 4: return launch_small<16>(a, s, mk);
+    case 5: return launch_small<32>(a, s, mk);
+    case 6: return launch_small<64>(a, s, mk);
+    case 7: return launch_small<128>(a, s, mk);
+    case 8: return launch_small<256>(a, s, mk);
+    case 9: return launch_small<512>(a, s, mk);
+    case 10: return launch_small<1024>(a, s, mk);
+    case 11: return launch_small<2048>(a, s, mk);
+    case 12: return launch_small<4096>(a, s, mk);
+    case 13: return launch_four_step<13>(p, a, s, mk);
+    case 14: return launch_four_step<14>(p, a, s, mk);
+    case 15: return launch_four_step<15>(p, a, s, mk);
+    case 16: return launch_four_step<16>(p, a, s, mk);
+    case 17: return launch_four_step<17>(p, a, s, mk);
+    case 18: return launch_four_step<18>(p, a, s, mk);
+    case 19: return launch_four_step<19>(p, a, s, mk);
+    case 20: return launch_four_step<20>(p, a, s, mk);
+    case 21: return launch_four_step<21>(p, a, s, mk);
+    case 22: return launch_four_step<22>(p, a, s, mk);
+    case 23: return launch_four_step<23>(p, a, s, mk);
     default: return cudaErrorInvalidValue;
   }
 }
 
+cudaError_t rhs_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s) { return rhs_launch_impl(p, a, s, nullptr); }
+
+cudaError_t rhs_launch_marked(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, cudaEvent_t* ev, int* cls, int cap,
+                              int* n) {
+  Marks mk{ev, cls, cap, 0};
+  cudaError_t e = rhs_launch_impl(p, a, s, &mk);
+  *n = mk.n;
+  return e;
+}
+
 template <int P>
 static cudaError_t smem_small() {
-  using PL = FftPlan<P, SmallCfg<P>::E>;
-  return cudaFuncSetAttribute(k_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(PL::SMEM * sizeof(double2)));
+  return cudaFuncSetAttribute(k_small<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg<P>::SMEM_BYTES);
+}
+
+template <typename CF>
+static cudaError_t smem_four_step_cf() {
+  cudaError_t e;
+  e = cudaFuncSetAttribute(k_col_fwd<CF::N1, CF::E1, CF::C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)CF::SM_COLFWD);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2, CF::ROW_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SM_ROW);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)CF::SM_COLINV);
 }
 
 template <int L>
 static cudaError_t smem_four_step() {
-  using CF = Cfg<L>;
-  cudaError_t e;
-  e = cudaFuncSetAttribute(k_col_fwd<CF::N1, CF::E1, CF::C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(CF::C * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2)));
+  cudaError_t e = smem_four_step_cf<Cfg<L>>();
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(2 * FftPlan<CF::N2, CF::E2>::SMEM * sizeof(double2)));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(CF::CP * FftPlan<CF::N1, CF::E1>::SMEM * sizeof(double2)));
+  if constexpr (L == 21) {
+#define AGK_X(id, e1, e2, c) \
+  if ((e = smem_four_step_cf<Cfg<21, e1, e2, c>>()) != cudaSuccess) return e;
+    AGK_L21_VARIANTS(AGK_X)
+#undef AGK_X
+  }
+  return e;
 }
 
 cudaError_t rhs_set_smem_limits() {
   cudaError_t e = cudaSuccess;
 #define AGK_TRY(x) \
   if ((e = (x)) != cudaSuccess) return e;
+  AGK_TRY(smem_small<1024>());
+  AGK_TRY(smem_small<2048>());
   AGK_TRY(smem_small<4096>());
-  AGK_TRY(smem_small<8192>());
+  AGK_TRY(smem_four_step<13>());
   AGK_TRY(smem_four_step<14>());
   AGK_TRY(smem_four_step<15>());
   AGK_TRY(smem_four_step<16>());

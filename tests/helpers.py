@@ -27,20 +27,7 @@ def factors(kind, m, alpha=0.0):
     raise ValueError(kind)
 
 
-def config4_inputs(m=1 << 20, r=16, seed=0x5EED5EED):
-    """BASELINE config 4: U_ia = u_a i^p_a, V_aj = v_a j^-p_a, n_s = exp(-s/1000) U(0.9,1.1)
-    (SURVEY §8d draw order: u_a, v_a then p_a per rank, then n)."""
-    rng = np.random.Generator(np.random.MT19937(seed))
-    u = np.empty(r)
-    v = np.empty(r)
-    p = np.empty(r)
-    for a in range(r):
-        u[a] = rng.uniform(0.5, 1.5)
-        v[a] = rng.uniform(0.5, 1.5)
-        p[a] = rng.uniform(-0.5, 0.5)
-    i = np.arange(1, m + 1, dtype=np.float64)
-    U = np.ascontiguousarray((u[None, :] * i[:, None] ** p[None, :]))
-    V = np.ascontiguousarray((v[:, None] * i[None, :] ** (-p[:, None])))
-    s = np.arange(1, m + 1, dtype=np.float64)
-    n = np.exp(-s / 1000.0) * rng.uniform(0.9, 1.1, size=m)
-    return U, V, n
+def config4_inputs(m=1 << 20, r=16):
+    """BASELINE config 4 inputs (paper_2407_16559_b200/configs.py, seed 0x5eed5eed)."""
+    from paper_2407_16559_b200.configs import random_config4
+    return random_config4(m, r)
