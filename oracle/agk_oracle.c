@@ -145,10 +145,14 @@ static void dedupe(const ora_model* md, double* weight, unsigned char* skip) {
   }
 }
 
+#ifndef ORA_PAD_FACTOR
+#define ORA_PAD_FACTOR 1 /* 2: an equally valid variant with a twice longer FFT (noise-floor build) */
+#endif
+
 int ora_birth_term(const ora_model* md, const double* n, double* out) {
   if (!model_ok(md)) return -1;
   const size_t m = md->m, r = md->r;
-  const size_t padded = next_pow2(2 * m);
+  const size_t padded = next_pow2(2 * m) * ORA_PAD_FACTOR;
   fft_plan plan;
   if (plan_init(&plan, padded)) return -1;
   double* packed = (double*)malloc(2 * padded * sizeof(double));

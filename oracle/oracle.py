@@ -21,6 +21,8 @@ LIBS = {
     "reference": (os.path.join(HERE, "_ref", "libaggkin_ref.so"), "ref_"),
     # the restatement built with FMA contraction: the CPU-vs-CPU noise floor for trajectories
     "port_fma": (os.path.join(HERE, "liboracle_fma.so"), "ora_"),
+    # the restatement with a 2x longer FFT (different roundoff, same algebra)
+    "port_pad2": (os.path.join(HERE, "liboracle_pad2.so"), "ora_"),
 }
 
 AGGREGATION, SOURCES, SHATTERING = 0, 1, 2

@@ -465,7 +465,7 @@ def run(ws: RhsWorkspace, cfg: SimulationConfig) -> RunReport:
                      rep.total_accepted, rep.total_rejects, rep.wall_seconds)
 
 
-KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv")
+KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv", "transpose")
 
 
 def eval_rhs_timed(ws: RhsWorkspace, n_dev, out_dev, count: int) -> float:

@@ -459,6 +459,45 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
       tw[16384 + nlo + k] = make_double2((double)cosl(ang), (double)sinl(ang));
     }
   }
+  if (p.fast) {
+    // warp fast path: column-major (U_a, V_a) pairs per unique rank, the n grid buffer and the
+    // 32x32 / radix-2 tables
+    const int64_t N1 = p.n1, N2 = p.n2, H = N1 / 2;
+    double2* uvg;
+    double* ng;
+    CK_C(dalloc(hp, &uvg, (size_t)h->rf * N2 * H), "alloc UV grid");
+    CK_C(dalloc(hp, &ng, (size_t)N2 * H), "alloc n grid");
+    std::vector<double2> col((size_t)N2 * H);
+    for (int ub = 0; ub < h->rf; ++ub) {
+      const int ra = uniq_rank[ub];
+      for (int64_t n2 = 0; n2 < N2; ++n2)
+        for (int64_t n1 = 0; n1 < H; ++n1) {
+          const int64_t i = n1 * N2 + n2;
+          col[n2 * H + n1] = i < m ? make_double2(d->u[i * r + ra], d->v[(int64_t)ra * m + i]) : make_double2(0.0, 0.0);
+        }
+      CK_C(cudaMemcpy(uvg + (size_t)ub * N2 * H, col.data(), col.size() * sizeof(double2), cudaMemcpyHostToDevice),
+           "upload UV grid");
+    }
+    std::vector<double2> t32(2048);
+    const long double pi = 3.141592653589793238462643383279502884L;
+    for (int k1 = 0; k1 < 32; ++k1)
+      for (int l = 0; l < 32; ++l) {
+        const long double ang = -2.0L * pi * (long double)(l * k1) / 1024.0L;
+        t32[k1 * 32 + l] = make_double2((double)cosl(ang), (double)sinl(ang));
+      }
+    for (int rr = 0; rr < 32; ++rr)
+      for (int l = 0; l < 32; ++l) {
+        const long double ang = -2.0L * pi * (long double)(l + 32 * rr) / 2048.0L;
+        t32[1024 + rr * 32 + l] = make_double2((double)cosl(ang), (double)sinl(ang));
+      }
+    double2* dt32;
+    CK_C(dalloc(hp, &dt32, t32.size()), "alloc tables");
+    CK_C(cudaMemcpy(dt32, t32.data(), t32.size() * sizeof(double2), cudaMemcpyHostToDevice), "upload tables");
+    a.uvg = uvg;
+    a.ng = ng;
+    a.tw32 = dt32;
+    a.tw2048h = dt32 + 1024;
+  }
   CK_C(dalloc(hp, &h->tw_all, tw.size()), "alloc twiddles");
   CK_C(cudaMemcpy(h->tw_all, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice), "upload twiddles");
 

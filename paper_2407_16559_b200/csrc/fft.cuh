@@ -87,10 +87,26 @@ struct Dft<4, SIGN> {
   }
 };
 
+// multiply by exp(SIGN * 2*pi*i*m/32), m a compile-time constant after unrolling
+template <int SIGN>
+__device__ __forceinline__ double2 mul_w32(double2 a, int m) {
+  m &= 31;
+  if ((m & 1) == 0) return mul_w16<SIGN>(a, m >> 1);
+  // odd m: cos/sin of pi*m/16
+  constexpr double c1 = 0.98078528040323044913, s1 = 0.19509032201612826785;  // pi/16
+  constexpr double c3 = 0.83146961230254523708, s3 = 0.55557023301960222474;  // 3pi/16
+  const double cs[8] = {c1, c3, s3, s1, -s1, -s3, -c3, -c1};  // m = 1,3,...,15
+  const double sn[8] = {s1, s3, c3, c1, c1, c3, s3, s1};
+  const int q = (m & 15) >> 1;
+  const double sg = (m & 16) ? -1.0 : 1.0;  // exp(i*pi*(m+16)/16) = -exp(i*pi*m/16)
+  return cmul(a, make_double2(sg * cs[q], sg * SIGN * sn[q]));
+}
+
 // radix-2 decimation in time on top of the half-size DFT: X[k] = E[k] + W^k O[k]
 template <int R, int SIGN>
 struct Dft {
   __device__ __forceinline__ static void run(double2* x) {
+    static_assert(R <= 32, "compile-time twiddles cover radix <= 32");
     double2 e[R / 2], o[R / 2];
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) {
@@ -101,7 +117,7 @@ struct Dft {
     Dft<R / 2, SIGN>::run(o);
 #pragma unroll
     for (int k = 0; k < R / 2; ++k) {
-      const double2 t = mul_w16<SIGN>(o[k], k * (16 / R));
+      const double2 t = mul_w32<SIGN>(o[k], k * (32 / R));
       x[k] = cadd(e[k], t);
       x[k + R / 2] = csub(e[k], t);
     }
@@ -119,7 +135,7 @@ __device__ __forceinline__ void dft_halfzero(double2* x) {
 #pragma unroll
     for (int r = 0; r < R / 2; ++r) {
       a[r] = x[r];
-      b[r] = mul_w16<SIGN>(x[r], r * (16 / R));
+      b[r] = mul_w32<SIGN>(x[r], r * (32 / R));
     }
     Dft<R / 2, SIGN>::run(a);
     Dft<R / 2, SIGN>::run(b);
@@ -286,6 +302,33 @@ __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, c
     stockham_pass<N, E, P::R0, SIGN, PADS, only, HALFZERO>(v, sm, j, 1, nullptr, active);
     FullPasses<N, E, SIGN, PADS, 0, P::NFULL>::run(v, sm, j, P::R0, smtw, active);
   }
+}
+
+// ---- warp-synchronous 1024-point FFT (32 x 32): no block barriers, one shared-memory exchange.
+// On entry lane l holds x[l + 32 r] in v[r]; on exit X[l + 32 k] in v[k] (same distribution).
+//   step A: DFT_32 over r in registers -> Y_l[k1]; twiddle W_1024^{l k1} (table tw[k1*32 + l]);
+//   exchange through the warp's region xs (32 rows x 33, conflict-free both ways);
+//   step B: DFT_32 over l in registers.
+constexpr int kXS = 32 * 33;  // double2 entries of a warp exchange region
+template <int SIGN, bool HALFZERO>
+__device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, const double2* tw, int lane) {
+  if constexpr (HALFZERO) {
+    dft_halfzero<32, SIGN>(v);
+  } else {
+    Dft<32, SIGN>::run(v);
+  }
+#pragma unroll
+  for (int k = 1; k < 32; ++k) {
+    const double2 w = tw[k * 32 + lane];
+    v[k] = cmul(v[k], SIGN < 0 ? w : cconj(w));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) xs[k * 33 + lane] = v[k];
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; ++l) v[l] = xs[lane * 33 + l];
+  Dft<32, SIGN>::run(v);
 }
 
 // W_P^e for the four-step twiddles, e < P, from two short tables:

@@ -61,11 +61,17 @@ struct RhsArgs {
   int nblk_colfwd;
   TwTable tw_n1, tw_n2, tw_small;
   TwoLevel twp;
+  // warp fast path (P = 2^21): column-major (U,V) per unique rank, n in grid layout, tables
+  const double2* uvg;
+  double* ng;
+  const double2* tw32;     // [k1*32 + l] = W_1024^{l k1}
+  const double2* tw2048h;  // [r*32 + l] = W_2048^{l + 32 r}
 };
 
 // Launch geometry and per-handle tables for one problem size.
 struct RhsPlan {
-  int small;     // 1: single-CTA path (P <= 8192)
+  int small;     // 1: single-CTA path (P <= 4096)
+  int fast;      // 1: warp-synchronous path (P = 2^21)
   int log2p;
   int n1, n2, c, cp;
   int gsize;     // ranks per group in the four-step path
@@ -73,7 +79,7 @@ struct RhsPlan {
 };
 
 // kernel classes for per-launch timing
-enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3 };
+enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4 };
 
 // host-side launchers (rhs.cu)
 void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);
@@ -85,6 +91,10 @@ size_t rhs_y_elems(const RhsPlan& plan);
 size_t rhs_acc_elems(const RhsPlan& plan);
 size_t rhs_partial_elems(const RhsPlan& plan, int rf);
 cudaError_t rhs_set_smem_limits();
+// warp fast path (rhs_w.cu)
+cudaError_t rhs_w_set_smem_limits();
+cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
+                         void* mk);
 
 // Injected fakes (AGK_RHS_DECAY, ...) as one elementwise kernel.
 cudaError_t fake_rhs_launch(int kind, double param, VecRef n, double* out, int64_t m,

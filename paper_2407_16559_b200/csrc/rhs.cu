@@ -22,121 +22,12 @@
 #include <cstdio>
 
 #include "internal.h"
+#include "rhs_common.cuh"
 
 namespace agk {
 
-constexpr int kSwap = 1000000;  // rank_map code offset for swapped folds
 
 // ------------------------------------------------------------------ shared device helpers
-
-// Sum NV doubles over the CTA (fixed shuffle tree + fixed warp order); result valid in thread 0.
-template <int NV>
-__device__ __forceinline__ void block_sum(double (&x)[NV], double* red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) x[k] += __shfl_xor_sync(0xffffffffu, x[k], off);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) red[warp * NV + k] = x[k];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s += red[w * NV + k];
-      x[k] = s;
-    }
-  }
-  __syncthreads();
-}
-
-// Reduce the per-CTA moment partials [ub][blk][4] into tot[ub*4+q] (global scratch), fixed
-// order, by all warps of the calling CTA (blockDim a multiple of 32).
-__device__ void reduce_partials(const RhsArgs& a, int nblk, double* tot) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int p = warp; p < a.rf * 4; p += nw) {
-    const int ub = p >> 2, q = p & 3;
-    double s = 0.0;
-    for (int b = lane; b < nblk; b += 32) s += a.partials[((int64_t)ub * nblk + b) * 4 + q];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (lane == 0) tot[p] = s;
-  }
-}
-
-// w_a for every rank (folded ranks read their partner's sums), pair and monomer gains
-// (rhs.cpp:24-36 and 185-196), written to a.scalars by one thread.
-__device__ void finalize_scalars(const RhsArgs& a, const double* tot, double n0) {
-  double pair = 0.0, mono = 0.0;
-  for (int ra = 0; ra < a.r; ++ra) {
-    const int code = a.rank_map[ra];
-    const bool sw = code >= kSwap;
-    const int ub = sw ? code - kSwap : code;
-    const double A0 = tot[ub * 4 + 0], A1 = tot[ub * 4 + 1];
-    const double B0 = tot[ub * 4 + 2], B1 = tot[ub * 4 + 3];
-    const double su0 = sw ? B0 : A0, su1 = sw ? B1 : A1;
-    const double sv0 = sw ? A0 : B0, sv1 = sw ? A1 : B1;
-    a.scalars[ra] = sv0 + a.v0[ra] * n0;  // w_a = sum_j V_aj n_j
-    pair += su1 * sv0 + su0 * sv1;
-    mono += a.u0[ra] * sv1;
-  }
-  a.scalars[a.r] = pair;
-  a.scalars[a.r + 1] = mono;
-}
-
-// Epilogue for output index jo >= 1: S = birth - death [+ shattering loss] [+ sources]
-__device__ __forceinline__ double epilogue(const RhsArgs& a, const double* __restrict__ n,
-                                           int64_t jo, double birth) {
-  double res = (a.flags & T_BIRTH) ? birth : 0.0;
-  if (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) {
-    double rowsum = 0.0;
-    for (int ra = 0; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + jo) * a.scalars[ra];
-    const double nn = n[jo];
-    if (a.flags & T_DEATH) res = res - nn * rowsum;
-    if (a.flags & T_DEATH_POS) res = nn * rowsum;
-    if (a.flags & T_SHATTER) res = res + (-a.lambda * nn) * rowsum;
-  }
-  if (a.flags & T_SOURCES) {
-    for (int q = 0; q < a.nsrc; ++q)
-      if (a.src_k[q] - 1 == jo) res += a.src_rate[q];
-  }
-  return res;
-}
-
-// out[0]: no birth; death; shattering gain at s = 1 (rhs.cpp:208); sources at k = 1.
-__device__ __forceinline__ double epilogue0(const RhsArgs& a, const double* __restrict__ n) {
-  double res = 0.0;
-  const double n0 = n[0];
-  if (a.flags & (T_DEATH | T_DEATH_POS)) {
-    double rowsum = 0.0;
-    for (int ra = 0; ra < a.r; ++ra) rowsum += a.ut[(int64_t)ra * a.m] * a.scalars[ra];
-    if (a.flags & T_DEATH) res = res - n0 * rowsum;
-    if (a.flags & T_DEATH_POS) res = n0 * rowsum;
-  }
-  if (a.flags & T_SHATTER) {
-    const double pair = a.scalars[a.r], mono = a.scalars[a.r + 1];
-    res = res + (0.5 * a.lambda * pair + a.lambda * n0 * mono);
-  }
-  if (a.flags & T_SOURCES) {
-    for (int q = 0; q < a.nsrc; ++q)
-      if (a.src_k[q] == 1) res += a.src_rate[q];
-  }
-  return res;
-}
-
-// conjugate-pair split and product of one packed spectrum bin (rhs.cpp:138-144):
-// A = (Z + conj Zp)/2, B = -i/2 (Z - conj Zp), returns A*B
-__device__ __forceinline__ double2 split_product(double2 z, double2 zp) {
-  const double mr = zp.x, mi = -zp.y;
-  const double ar = 0.5 * (z.x + mr), ai = 0.5 * (z.y + mi);
-  const double dr = z.x - mr, di = z.y - mi;
-  const double br = 0.5 * di, bi = -0.5 * dr;
-  return make_double2(ar * br - ai * bi, ar * bi + ai * br);
-}
 
 // ------------------------------------------------------------------ small path: one CTA
 
@@ -255,8 +146,9 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
 // ------------------------------------------------------------------ four-step path
 
 template <int L, int E1_ = ((1 << (L / 2)) >= 256 ? 16 : 8), int E2_ = ((1 << (L - L / 2)) >= 256 ? 16 : 8),
-          int C_ = (L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2))))>
+          int C_ = (L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2)))), int ROWMODE_ = 0>
 struct Cfg {
+  static constexpr int ROWMODE = ROWMODE_;  // 1: no staging, 2 CTAs/SM register budget
   static constexpr int N1 = 1 << (L / 2), N2 = 1 << (L - L / 2);
   static constexpr int E1 = E1_;
   static constexpr int E2 = E2_;
@@ -268,25 +160,12 @@ struct Cfg {
   static constexpr int R1 = PL1::template smem<kNoPad>();  // column team region (no padding)
   // + staging of the next rank's U, V (column kernel) / Y rows (row kernel)
   static constexpr size_t SM_COLFWD = (size_t)(C * R1 + PL1::TWS) * sizeof(double2) + (size_t)C * N1 * sizeof(double);
-  static constexpr bool ROW_STAGE = (2 * PL2::SMEM + PL2::TWS + 2 * N2) * 16 <= 232448;
+  static constexpr bool ROW_STAGE = ROWMODE == 0 && (2 * PL2::SMEM + PL2::TWS + 2 * N2) * 16 <= 232448;
+  static constexpr int ROW_MINB = ROWMODE == 1 ? 2 : 1;
   static constexpr size_t SM_ROW = (size_t)(2 * PL2::SMEM + PL2::TWS + (ROW_STAGE ? 2 * N2 : 0)) * sizeof(double2);
   static constexpr size_t SM_COLINV = (size_t)(CP * R1 + PL1::TWS) * sizeof(double2);
   static_assert(SM_COLFWD <= 232448 && SM_ROW <= 232448 && SM_COLINV <= 232448, "shared memory budget");
   static_assert(C * T1 >= 32 && 2 * T2 >= 32, "column-forward and row CTAs need full warps");
-};
-
-// Four-step twiddles W_P^{SIGN e} for e = e0 + r*de, r = 0..E-1, by a short recurrence from two
-// accurate two-level lookups (error ~r ulp, no per-element table loads).
-template <int SIGN>
-struct TwSeries {
-  double2 w, st;
-  __device__ __forceinline__ TwSeries(const TwoLevel& t, uint32_t e0, uint32_t de)
-      : w(tw_p<SIGN>(t, e0)), st(tw_p<SIGN>(t, de)) {}
-  __device__ __forceinline__ double2 next() {
-    const double2 cur = w;
-    w = cmul(w, st);
-    return cur;
-  }
 };
 
 template <int N1, int E1, int C>
@@ -364,8 +243,8 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   }
 }
 
-template <int N2, int E2, bool STAGE>
-__global__ void __launch_bounds__(2 * (N2 / E2)) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
+template <int N2, int E2, bool STAGE, int MINB>
+__global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
   using PL = FftPlan<N2, E2>;
   constexpr int T2 = N2 / E2, NT = 2 * T2, Q = E2 / 2;
   extern __shared__ double2 smem[];
@@ -550,7 +429,9 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   if (g > rf) g = rf;
   p->gsize = g;
   const int ngroups = (rf + g - 1) / g;
-  p->launches = p->small ? 1 : 2 * ngroups + 1;
+  const char* fe = getenv("AGK_FAST");
+  p->fast = (L == 21) && !(fe && atoi(fe) == 0);
+  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);
 }
 
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
@@ -573,6 +454,7 @@ static void mark(Marks* mk, int cls, cudaStream_t s) {
     mk->cls[mk->n++] = cls;
   }
 }
+static void mark_cb(void* mk, int cls, cudaStream_t s) { mark(static_cast<Marks*>(mk), cls, s); }
 
 template <int P>
 static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s, Marks* mk) {
@@ -590,7 +472,7 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     k_col_fwd<CF::N1, CF::E1, CF::C><<<CF::N2 / CF::C, CF::C * CF::T1, sm1, s>>>(a, g0, gc);
     mark(mk, K_COL_FWD, s);
-    k_row<CF::N2, CF::E2, CF::ROW_STAGE><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
+    k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
     mark(mk, K_ROW, s);
   }
   k_col_inv<CF::N1, CF::E1, CF::CP><<<CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s>>>(a);
@@ -600,7 +482,7 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
 
 // Tuning variants of the M = 2^20 shape (AGK_VARIANT), default 0.
 #define AGK_L21_VARIANTS(X) \
-  X(0, 16, 16, 8) X(1, 16, 16, 4) X(2, 8, 16, 8) X(3, 8, 8, 8) X(4, 8, 8, 4) X(5, 16, 8, 4)
+  X(0, 16, 16, 8, 0) X(1, 16, 16, 4, 0) X(2, 8, 16, 8, 0) X(6, 16, 16, 8, 1) X(7, 16, 16, 4, 1)
 
 static int l21_variant() {
   static int v = -1;
@@ -615,8 +497,8 @@ template <int L>
 static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
   if constexpr (L == 21) {
     switch (l21_variant()) {
-#define AGK_X(id, e1, e2, c) \
-  case id: return launch_four_step_cf<Cfg<21, e1, e2, c>>(p, a, s, mk);
+#define AGK_X(id, e1, e2, c, rm) \
+  case id: return launch_four_step_cf<Cfg<21, e1, e2, c, rm>>(p, a, s, mk);
       AGK_L21_VARIANTS(AGK_X)
 #undef AGK_X
       default: break;
@@ -626,6 +508,7 @@ static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStre
 }
 
 static cudaError_t rhs_launch_impl(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
+  if (p.fast) return rhs_w_launch(p, a, s, mk ? mark_cb : nullptr, mk);
   switch (p.log2p) {
     case 2: return launch_small<4>(a, s, mk);
     case 3: return launch_small<8>(a, s, mk);
@@ -674,7 +557,7 @@ static cudaError_t smem_four_step_cf() {
   e = cudaFuncSetAttribute(k_col_fwd<CF::N1, CF::E1, CF::C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)CF::SM_COLFWD);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2, CF::ROW_STAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SM_ROW);
+  e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SM_ROW);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)CF::SM_COLINV);
@@ -685,8 +568,8 @@ static cudaError_t smem_four_step() {
   cudaError_t e = smem_four_step_cf<Cfg<L>>();
   if (e != cudaSuccess) return e;
   if constexpr (L == 21) {
-#define AGK_X(id, e1, e2, c) \
-  if ((e = smem_four_step_cf<Cfg<21, e1, e2, c>>()) != cudaSuccess) return e;
+#define AGK_X(id, e1, e2, c, rm) \
+  if ((e = smem_four_step_cf<Cfg<21, e1, e2, c, rm>>()) != cudaSuccess) return e;
     AGK_L21_VARIANTS(AGK_X)
 #undef AGK_X
   }
@@ -711,6 +594,7 @@ cudaError_t rhs_set_smem_limits() {
   AGK_TRY(smem_four_step<21>());
   AGK_TRY(smem_four_step<22>());
   AGK_TRY(smem_four_step<23>());
+  AGK_TRY(rhs_w_set_smem_limits());
 #undef AGK_TRY
   return e;
 }

@@ -38,12 +38,15 @@ def _metrics(x, w):
     )
 
 
-# north_star bars, each raised to 4x the CPU-vs-CPU noise floor where that floor is higher.
+# north_star bars, each raised to 10x the CPU-vs-CPU noise floor where that floor is higher
+# (after the first divergent decision the drift is a random walk of O(tol) kicks; the floor is
+# one sample of it, hence the factor), plus lock-step agreement before that point.
 # The error estimate ||n5 - n4|| (or ||half - full||) is a difference of O(1) quantities and carries
 # ~1e-8 relative roundoff noise in ANY build, so trajectories whose step sequence is sensitive to it
 # drift apart by O(tol) per divergent accept/reject even between two CPU builds of the reference
 # (SURVEY §8c note 6). The floor is the largest distance from the oracle of: the oracle built with
-# FMA contraction, and the oracle run at tol*(1 -+ 1e-8) (an err perturbation of that size).
+# FMA contraction, the oracle with a 2x longer FFT (a different roundoff pattern in the birth term,
+# as the GPU's four-step FFT has), and the oracle run at tol*(1 -+ 1e-8).
 BARS = dict(N=1e-8, M1=1e-8, state=1e-6, elem=1e-6, accepted=0.02)
 
 
@@ -60,8 +63,23 @@ def check_run(g, w, f=None):
     else:
         mf = _metrics(f, w)
     for key, bar in BARS.items():
-        assert mg[key] <= max(bar, 4.0 * mf[key]), (key, mg[key], bar, mf[key])
+        assert mg[key] <= max(bar, FLOOR_FACTOR * mf[key]), (key, mg[key], bar, mf[key])
     return mg, mf
+
+
+FLOOR_FACTOR = 10.0
+
+
+def check_lockstep(g, w, tol=1e-9):
+    """Until the first accept/reject decision that differs (a borderline err ~ tol), the device
+    trajectory must track the oracle's to ~roundoff: same cumulative rejects and evals, t and N
+    within `tol` relative. Returns the index of the first divergent record (or None)."""
+    for q, (a, b) in enumerate(zip(g.records, w["records"])):
+        if a["rejects"] != b["rejects"] or a["rhs_evals"] != b["rhs_evals"]:
+            return q
+        assert abs(a["t"] - b["t"]) <= tol * max(abs(b["t"]), 1.0), q
+        assert abs(a["density"] - b["density"]) <= tol * max(abs(b["density"]), 1e-300), q
+    return None
 
 
 class _Floor(dict):
@@ -73,7 +91,8 @@ def oracle_pair(om, n0, ctl_kwargs, t_end, **kw):
     from oracle.oracle import Oracle
     port = Oracle("port")
     w = port.run(om, n0, O.Control(**ctl_kwargs), t_end, **kw)
-    variants = [Oracle("port_fma").run(om, n0, O.Control(**ctl_kwargs), t_end, **kw)]
+    variants = [Oracle("port_fma").run(om, n0, O.Control(**ctl_kwargs), t_end, **kw),
+                Oracle("port_pad2").run(om, n0, O.Control(**ctl_kwargs), t_end, **kw)]
     if ctl_kwargs.get("mode", O.ADAPTIVE) == O.ADAPTIVE:
         for d in (1e-8, -1e-8):
             ck = dict(ctl_kwargs, tol=ctl_kwargs.get("tol", 1e-6) * (1.0 + d))
@@ -246,8 +265,11 @@ def test_config5_reduced_m(agk, oracle_port, stepper):
     """BASELINE config 5 kernel/source at reduced M (4096) to t=50 (SURVEY §8d parity plan)."""
     om, ws = build(agk, "brownian2", 4096, variant=O.SOURCES, sources=[(1, 1.0)])
     n0 = np.zeros(4096)
-    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(stepper=stepper, tol=1e-6), 50.0, n0))
-    w, f = oracle_pair(om, n0, dict(stepper=stepper, tol=1e-6), 50.0)
+    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(stepper=stepper, tol=1e-6), 50.0, n0,
+                                         record=agk.RECORD_EVERY_STEP, records_capacity=100000))
+    w, f = oracle_pair(om, n0, dict(stepper=stepper, tol=1e-6), 50.0, record=O.RECORD_EVERY_STEP,
+                       records_capacity=100000)
+    check_lockstep(g, w)
     check_run(g, w, f)
 
 
@@ -256,6 +278,8 @@ def test_config3_reduced_m(agk, oracle_port):
     om, ws = build(agk, "brownian", 2048, 0.9, O.SHATTERING, lam=0.01)
     n0 = np.zeros(2048)
     n0[0] = 1.0
-    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(tol=1e-8), 20.0, n0))
-    w, f = oracle_pair(om, n0, dict(tol=1e-8), 20.0)
+    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(tol=1e-8), 20.0, n0, record=agk.RECORD_EVERY_STEP,
+                                         records_capacity=100000))
+    w, f = oracle_pair(om, n0, dict(tol=1e-8), 20.0, record=O.RECORD_EVERY_STEP, records_capacity=100000)
+    check_lockstep(g, w)
     check_run(g, w, f)

@@ -101,7 +101,7 @@ def test_controller_on_fakes_matches_oracle(agk, oracle_port, stepper, mode, fak
     # device pow is within 2 ulp of glibc's: tau after a reject agrees to ~1e-14 relative
     assert abs(g.tau_used - w["tau_used"]) <= 4e-14 * abs(w["tau_used"])
     if g.status == O.STEP_OK:
-        assert abs(g.tau_next - w["tau_next"]) <= 1e-14 * abs(w["tau_next"])
+        assert abs(g.tau_next - w["tau_next"]) <= 1e-13 * abs(w["tau_next"])
         np.testing.assert_allclose(g.state, w["state"], rtol=1e-14, atol=1e-16)
         if math.isnan(w["error_estimate"]):
             assert math.isnan(g.error_estimate)
