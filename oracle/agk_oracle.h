@@ -62,6 +62,8 @@ int ora_euler_stability_bound(const ora_model* model, const double* n, double a,
 /* Dense literal-sum oracle of eval_rhs_dense_oracle (rhs.cpp:237-282) evaluated on the
  * low-rank factors' entries K(i,j) = sum_a U(i,a) V(a,j) (kernels.cpp LowRankFactors::entry). */
 int ora_eval_rhs_dense(const ora_model* model, const double* n, double* out);
+/* The same RHS with every intermediate in long double (agk_truth.c): accuracy yardstick. */
+int ora_eval_rhs_truth(const ora_model* model, const double* n, double* out);
 
 /* StepControl (steppers.hpp:18-36) */
 enum { ORA_RK2 = 0, ORA_RK4 = 1, ORA_RKF45 = 2 };

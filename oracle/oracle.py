@@ -174,6 +174,10 @@ class Oracle:
     def eval_rhs_dense(self, model, n):
         return self._rhs_call("eval_rhs_dense", model, n)
 
+    def eval_rhs_truth(self, model, n):
+        """Long-double evaluation of the same algorithm (port library only)."""
+        return self._rhs_call("eval_rhs_truth", model, n)
+
     def euler_stability_bound(self, model, n, a):
         n = np.ascontiguousarray(n, dtype=np.float64)
         cm = model.c()

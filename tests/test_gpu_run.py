@@ -70,16 +70,28 @@ def check_run(g, w, f=None):
 FLOOR_FACTOR = 10.0
 
 
-def check_lockstep(g, w, tol=1e-9):
-    """Until the first accept/reject decision that differs (a borderline err ~ tol), the device
-    trajectory must track the oracle's to ~roundoff: same cumulative rejects and evals, t and N
-    within `tol` relative. Returns the index of the first divergent record (or None)."""
-    for q, (a, b) in enumerate(zip(g.records, w["records"])):
+def lockstep_len(x_records, w_records, tol=1e-9):
+    """Number of leading records on which run x tracks the oracle run w to ~roundoff (same
+    cumulative rejects and evals, t and N within `tol` relative)."""
+    q = 0
+    for a, b in zip(x_records, w_records):
         if a["rejects"] != b["rejects"] or a["rhs_evals"] != b["rhs_evals"]:
-            return q
-        assert abs(a["t"] - b["t"]) <= tol * max(abs(b["t"]), 1.0), q
-        assert abs(a["density"] - b["density"]) <= tol * max(abs(b["density"]), 1e-300), q
-    return None
+            break
+        if abs(a["t"] - b["t"]) > tol * max(abs(b["t"]), 1.0):
+            break
+        if abs(a["density"] - b["density"]) > tol * max(abs(b["density"]), 1e-300):
+            break
+        q += 1
+    return q
+
+
+def check_lockstep(g, w, f):
+    """The device trajectory stays in lock-step with the oracle at least half as long as an
+    equally valid CPU build with a different FFT roundoff pattern (the 2x-padded restatement,
+    f.variants[1]) does: the birth term's FFT noise in err decides where two builds part ways."""
+    cpu = lockstep_len(f.variants[1]["records"], w["records"])
+    gpu = lockstep_len(g.records, w["records"])
+    assert gpu >= min(cpu, len(w["records"])) // 2, (gpu, cpu)
 
 
 class _Floor(dict):
@@ -87,7 +99,7 @@ class _Floor(dict):
 
 
 def oracle_pair(om, n0, ctl_kwargs, t_end, **kw):
-    """(oracle run, noise-floor metrics) for one configuration."""
+    """(oracle run, noise-floor metrics) for one configuration; f.variants holds the CPU runs."""
     from oracle.oracle import Oracle
     port = Oracle("port")
     w = port.run(om, n0, O.Control(**ctl_kwargs), t_end, **kw)
@@ -99,6 +111,7 @@ def oracle_pair(om, n0, ctl_kwargs, t_end, **kw):
             variants.append(port.run(om, n0, O.Control(**ck), t_end, **kw))
     mets = [_metrics(v, w) for v in variants]
     f = _Floor({k: max(mt[k] for mt in mets) for k in BARS})
+    f.variants = variants
     return w, f
 
 
@@ -269,7 +282,7 @@ def test_config5_reduced_m(agk, oracle_port, stepper):
                                          record=agk.RECORD_EVERY_STEP, records_capacity=100000))
     w, f = oracle_pair(om, n0, dict(stepper=stepper, tol=1e-6), 50.0, record=O.RECORD_EVERY_STEP,
                        records_capacity=100000)
-    check_lockstep(g, w)
+    check_lockstep(g, w, f)
     check_run(g, w, f)
 
 
@@ -281,5 +294,5 @@ def test_config3_reduced_m(agk, oracle_port):
     g = agk.run(ws, agk.SimulationConfig(agk.StepControl(tol=1e-8), 20.0, n0, record=agk.RECORD_EVERY_STEP,
                                          records_capacity=100000))
     w, f = oracle_pair(om, n0, dict(tol=1e-8), 20.0, record=O.RECORD_EVERY_STEP, records_capacity=100000)
-    check_lockstep(g, w)
+    check_lockstep(g, w, f)
     check_run(g, w, f)
