@@ -53,33 +53,21 @@ def parse():
 
 
 # ------------------------------------------------------------------ distributed plumbing
+# replicas only (paper_2407_16559_b200/replicas.py): barrier + max over ranks, no data exchange
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+    from paper_2407_16559_b200 import replicas
+    return replicas.setup("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
 
 
 def barrier(world):
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    from paper_2407_16559_b200 import replicas
+    replicas.barrier(world)
 
 
 def max_over_ranks(x, world, local):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2407_16559_b200 import replicas
+    return replicas.max_over_ranks(x, world, local)
 
 
 # ------------------------------------------------------------------ clocks
@@ -359,9 +347,8 @@ def main():
         res = run_b200(args, world, rank, local)
     if rank == 0 and res is not None:
         print(json.dumps(res), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    from paper_2407_16559_b200 import replicas
+    replicas.teardown(world)
 
 
 if __name__ == "__main__":
