@@ -493,6 +493,12 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
     double2* dt32;
     CK_C(dalloc(hp, &dt32, t32.size()), "alloc tables");
     CK_C(cudaMemcpy(dt32, t32.data(), t32.size() * sizeof(double2), cudaMemcpyHostToDevice), "upload tables");
+    double* dvec;
+    CK_C(dalloc(hp, &dvec, (size_t)m), "alloc D");
+    a.dvec = dvec;
+    CK_C(cudaStreamCreateWithFlags(&h->plan.side, cudaStreamNonBlocking), "side stream");
+    CK_C(cudaEventCreateWithFlags(&h->plan.ev_fork, cudaEventDisableTiming), "event");
+    CK_C(cudaEventCreateWithFlags(&h->plan.ev_join, cudaEventDisableTiming), "event");
     a.uvg = uvg;
     a.ng = ng;
     a.tw32 = dt32;
@@ -569,6 +575,9 @@ void agk_rhs_destroy(agk_rhs* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->rhs_graph) cudaGraphExecDestroy(h->rhs_graph);
   for (void* p : h->allocs) cudaFree(p);
+  if (h->plan.side) cudaStreamDestroy(h->plan.side);
+  if (h->plan.ev_fork) cudaEventDestroy(h->plan.ev_fork);
+  if (h->plan.ev_join) cudaEventDestroy(h->plan.ev_join);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);

@@ -66,6 +66,8 @@ struct RhsArgs {
   double* ng;
   const double2* tw32;     // [k1*32 + l] = W_1024^{l k1}
   const double2* tw2048h;  // [r*32 + l] = W_2048^{l + 32 r}
+  double* dvec;            // m: the non-birth part of S (death, sources, shattering), side stream
+  int dbg;                 // experiment switches (AGK_DBG), 0 in production
 };
 
 // Launch geometry and per-handle tables for one problem size.
@@ -76,6 +78,10 @@ struct RhsPlan {
   int n1, n2, c, cp;
   int gsize;     // ranks per group in the four-step path
   int launches;  // kernels per RHS
+  // fast path: side stream + fork/join events (the death / row-sum pass runs concurrently with
+  // the row transforms)
+  cudaStream_t side;
+  cudaEvent_t ev_fork, ev_join;
 };
 
 // kernel classes for per-launch timing

@@ -145,8 +145,10 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
 
 // ------------------------------------------------------------------ four-step path
 
-template <int L, int E1_ = ((1 << (L / 2)) >= 256 ? 16 : 8), int E2_ = ((1 << (L - L / 2)) >= 256 ? 16 : 8),
-          int C_ = (L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2)))), int ROWMODE_ = 0>
+// Defaults: 4 points per thread up to P = 2^20 (latency-bound sizes want more warps; measured
+// 2x faster than 16 at P = 2^17, 2^18), 16 above.
+template <int L, int E1_ = (L <= 20 ? 4 : 16), int E2_ = (L <= 20 ? 4 : 16),
+          int C_ = (L <= 20 ? 4 : (L <= 21 ? 8 : 2)), int ROWMODE_ = 0>
 struct Cfg {
   static constexpr int ROWMODE = ROWMODE_;  // 1: no staging, 2 CTAs/SM register budget
   static constexpr int N1 = 1 << (L / 2), N2 = 1 << (L - L / 2);
@@ -418,7 +420,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->n1 = 1 << (p->log2p / 2);
   p->n2 = 1 << (p->log2p - p->log2p / 2);
   const int L = p->log2p;
-  p->c = L <= 13 ? 4 : (L <= 16 ? 2 : (L <= 18 ? 4 : (L <= 21 ? 8 : 2)));
+  p->c = L <= 20 ? 4 : (L <= 21 ? 8 : 2);
   p->cp = p->c / 2 > 0 ? p->c / 2 : 1;
   // Ranks per group: all unique ranks in one column/row launch pair (measured fastest at
   // M = 2^20, R = 16: the per-group intermediate then streams through HBM, but the launches and
@@ -427,11 +429,15 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   if (const char* env = getenv("AGK_RANK_GROUP")) g = atoi(env);
   if (g < 1) g = 1;
   if (g > rf) g = rf;
+  const char* fe0 = getenv("AGK_FAST");
+  if (L == 21 && !(fe0 && atoi(fe0) == 0) && g > 16) g = 16;  // warp path: <= 16 rank slots
   p->gsize = g;
   const int ngroups = (rf + g - 1) / g;
   const char* fe = getenv("AGK_FAST");
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
-  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);
+  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 4 : 0);
+  p->side = nullptr;
+  p->ev_fork = p->ev_join = nullptr;
 }
 
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
@@ -493,8 +499,30 @@ static int l21_variant() {
   return v;
 }
 
+// Mid-size variants (AGK_MVAR) for 2^14 <= P <= 2^20: fewer points per thread = more warps.
+#define AGK_MID_VARIANTS(X, L) \
+  X(1, L, 8, 8, 4) X(2, L, 4, 4, 4) X(3, L, 4, 8, 8) X(4, L, 8, 8, 8)
+
+static int mid_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AGK_MVAR");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int L>
 static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
+  if constexpr (L >= 16 && L <= 20) {
+    switch (mid_variant()) {
+#define AGK_M(id, LL, e1, e2, c) \
+  case id: return launch_four_step_cf<Cfg<LL, e1, e2, c, 0>>(p, a, s, mk);
+      AGK_MID_VARIANTS(AGK_M, L)
+#undef AGK_M
+      default: break;
+    }
+  }
   if constexpr (L == 21) {
     switch (l21_variant()) {
 #define AGK_X(id, e1, e2, c, rm) \
@@ -572,6 +600,12 @@ static cudaError_t smem_four_step() {
   if ((e = smem_four_step_cf<Cfg<21, e1, e2, c, rm>>()) != cudaSuccess) return e;
     AGK_L21_VARIANTS(AGK_X)
 #undef AGK_X
+  }
+  if constexpr (L >= 16 && L <= 20) {
+#define AGK_M(id, LL, e1, e2, c) \
+  if ((e = smem_four_step_cf<Cfg<LL, e1, e2, c, 0>>()) != cudaSuccess) return e;
+    AGK_MID_VARIANTS(AGK_M, L)
+#undef AGK_M
   }
   return e;
 }

@@ -51,11 +51,12 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gcount) {
+template <int kCW, bool STAGE>
+__global__ void __launch_bounds__(kCW * 32, STAGE ? 1 : 2) k_colw(RhsArgs a, int g0, int gcount) {
   extern __shared__ double2 smem[];
   double2* X = smem;                       // kCW exchange / output regions
-  double2* S = X + kCW * kXR;              // kCW staging regions (512 x (U,V))
-  double2* tw = S + kCW * kW_H;            // W_1024^{l k1}, [k1][l]
+  double2* S = X + kCW * kXR;              // kCW staging regions (512 x (U,V)), STAGE only
+  double2* tw = S + (STAGE ? kCW * kW_H : 0);  // W_1024^{l k1}, [k1][l]
   __shared__ double red[kCW][4];
   __shared__ double2 tk[kCW][32];  // four-step factors W_P^{32 n2 k} of the warp's column
   if (a.skip && *a.skip) return;
@@ -69,12 +70,14 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gco
   double2* Sw = S + w * kW_H;
   double2* Xw = X + w * kXR;
   auto prefetch = [&](int item) {
-    const int grp = item / gcount, ub = g0 + item % gcount;
-    const int n2 = grp * kCW + w;
-    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
+    if constexpr (STAGE) {
+      const int grp = item / gcount, ub = g0 + item % gcount;
+      const int n2 = grp * kCW + w;
+      const double2* src = a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
-    cp_async_commit();
+      for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
+      cp_async_commit();
+    }
   };
   if (it0 < it1) prefetch(it0);
   __syncthreads();
@@ -92,13 +95,16 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gco
       base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
       tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
     }
-    cp_async_wait_all();
-    __syncwarp();
+    if constexpr (STAGE) {
+      cp_async_wait_all();
+      __syncwarp();
+    }
+    const double2* uvsrc = STAGE ? Sw : a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
     double2 v[32];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const double2 uv = Sw[lane + 32 * r];
+      const double2 uv = uvsrc[lane + 32 * r];
       const double x = uv.x * nl[r], y = uv.y * nl[r];
       v[r] = make_double2(x, y);
       const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gco
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
-    warp_fft1024<-1, true>(v, Xw, tw, lane);
+    if (!(a.dbg & 1)) warp_fft1024<-1, true>(v, Xw, tw, lane);
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
 #pragma unroll
@@ -132,6 +138,7 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gco
     __syncthreads();
     // coalesced store of the tile: rows k1c, kCW consecutive columns
     double2* __restrict__ yg = a.y + (int64_t)g * P + (int64_t)grp * kCW;
+    if (!(a.dbg & 2))
     for (int idx = tid; idx < kW_N1 * kCW; idx += blockDim.x) {
       const int k1c = idx / kCW, ww = idx % kCW;
       yg[(int64_t)k1c * kW_N2 + ww] = X[ww * kXR + k1c];
@@ -148,7 +155,8 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colw(RhsArgs a, int g0, int gco
 // row pair (k1, N1-k1): warps (rho, h): rho = row, h = output parity of the radix-2 DIF split.
 // One CTA of 4 warps per SM; the next rank's two rows are staged by cp.async while this rank's
 // transforms run (the warp FFT keeps ~90% of its throughput at one warp per SMSP).
-__global__ void __launch_bounds__(128, 1) k_roww(RhsArgs a, int g0, int gcount, int first) {
+template <bool STAGE>
+__global__ void __launch_bounds__(128, STAGE ? 1 : 2) k_roww(RhsArgs a, int g0, int gcount, int first) {
   extern __shared__ double2 smem[];
   double2* X = smem;               // 4 regions
   double2* tw = X + 4 * kXR;       // W_1024^{l k1}, [k1][l]
@@ -161,6 +169,8 @@ __global__ void __launch_bounds__(128, 1) k_roww(RhsArgs a, int g0, int gcount, 
   const int nrows = n1 / 2 + 1;
   // items: (row pair k1, rank g), rank-minor; a CTA owns whole row pairs (acc in registers)
   auto prefetch = [&](int k1, int g) {
+    if constexpr (!STAGE) return;
+    if (a.dbg & 64) return;
     const double2* y0 = a.y + (int64_t)g * P + (int64_t)k1 * kW_N2;
     const double2* y1 = a.y + (int64_t)g * P + (int64_t)((n1 - k1) & (n1 - 1)) * kW_N2;
 #pragma unroll
@@ -184,12 +194,13 @@ __global__ void __launch_bounds__(128, 1) k_roww(RhsArgs a, int g0, int gcount, 
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + tid + 128 * j];
     for (int g = 0; g < gcount; ++g) {
       const double wt = a.uniq_weight[g0 + g];
-      cp_async_wait_all();
+      if constexpr (STAGE) { if (!(a.dbg & 64)) cp_async_wait_all(); }
       __syncthreads();  // staged rows visible; previous split done with X
       double2 v[32];
+      const double2* src = STAGE ? Sr : a.y + (int64_t)g * P + (int64_t)(rho == 0 ? k1 : (n1 - k1) & (n1 - 1)) * kW_N2;
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        const double2 lo = Sr[lane + 32 * r], hi = Sr[1024 + lane + 32 * r];
+        const double2 lo = src[lane + 32 * r], hi = src[1024 + lane + 32 * r];
         v[r] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), twh[r * 32 + lane]);
       }
       __syncthreads();  // everyone has read the staging buffer
@@ -198,11 +209,12 @@ __global__ void __launch_bounds__(128, 1) k_roww(RhsArgs a, int g0, int gcount, 
       } else if (k1 + (int)gridDim.x < nrows && gcount > 0) {
         prefetch(k1 + gridDim.x, 0);
       }
-      warp_fft1024<-1, false>(v, Xw, tw, lane);
+      if (!(a.dbg & 16)) warp_fft1024<-1, false>(v, Xw, tw, lane);
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];  // X_row[2(lane + 32k) + h]
       __syncthreads();
+      if (!(a.dbg & 32))
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int q = tid + 128 * j;
@@ -234,12 +246,6 @@ __global__ void __launch_bounds__(128) k_rowinvw(RhsArgs a) {
     tw[i] = __ldg(a.tw32 + i);
     twh[i] = __ldg(a.tw2048h + i);
   }
-  if (blockIdx.x == 0) {
-    double* tot = a.scalars + a.r + 2;
-    reduce_partials(a, a.nblk_colfwd, tot);
-    __syncthreads();
-    if (tid == 0) finalize_scalars(a, tot, a.n.get()[0]);
-  }
   __syncthreads();
   const int nrows = kW_N1 / 2 + 1;
   for (int k1b = 2 * blockIdx.x; k1b < nrows; k1b += 2 * gridDim.x) {
@@ -270,7 +276,30 @@ __global__ void __launch_bounds__(128) k_rowinvw(RhsArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(kCW * 32, 1) k_colinvw(RhsArgs a) {
+// w_a, pair and monomer gains from the column pass' partials (one CTA, fixed order)
+__global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
+  if (a.skip && *a.skip) return;
+  double* tot = a.scalars + a.r + 2;
+  reduce_partials(a, a.nblk_colfwd, tot);
+  __syncthreads();
+  if (threadIdx.x == 0) finalize_scalars(a, tot, a.n.get()[0]);
+}
+
+// The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
+// (rhs.cpp:24-46, 162-168, 170-210, 227-229). A pure stream over U (R x M) at full occupancy;
+// it runs on the side stream while the row transforms run.
+__global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
+  if (a.skip && *a.skip) return;
+  const double* __restrict__ n = a.n.get();
+  RhsArgs b = a;
+  b.flags = a.flags & ~T_BIRTH;
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < a.m; s += (int64_t)gridDim.x * blockDim.x)
+    a.dvec[s] = s == 0 ? epilogue0(b, n) : epilogue(b, n, s, 0.0);
+}
+
+// Inverse column pass: two real columns per complex 1024-pt inverse FFT, then S = birth + D.
+template <int kCW>
+__global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs a) {
   extern __shared__ double2 smem[];
   double2* X = smem;
   double2* tw = X + kCW * kXR;
@@ -279,8 +308,8 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colinvw(RhsArgs a) {
   for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
   __syncthreads();
   const double2* __restrict__ G = a.acc;
-  const double* __restrict__ n = a.n.get();
   const double scale = ldexp(0.5, -a.log2p);
+  const bool birth = (a.flags & T_BIRTH) != 0;
   double* tile = reinterpret_cast<double*>(X);  // [512][2 kCW + 1] birth values, after the FFTs
   constexpr int TS = 2 * kCW + 1;
   for (int grp = blockIdx.x; grp < kW_N2 / (2 * kCW); grp += gridDim.x) {
@@ -311,48 +340,92 @@ __global__ void __launch_bounds__(kCW * 32, 1) k_colinvw(RhsArgs a) {
     for (int idx = tid; idx < kW_H * 2 * kCW; idx += blockDim.x) {
       const int nn1 = idx / (2 * kCW), c = idx % (2 * kCW);
       const int64_t jo = (int64_t)nn1 * kW_N2 + grp * 2 * kCW + c + 1;
-      if (jo < a.m) a.out[jo] = epilogue(a, n, jo, tile[nn1 * TS + c]);
+      if (jo < a.m) a.out[jo] = (birth ? tile[nn1 * TS + c] : 0.0) + a.dvec[jo];
     }
-    if (grp == 0 && tid == 0) a.out[0] = epilogue0(a, n);
+    if (grp == 0 && tid == 0) a.out[0] = a.dvec[0];
     __syncthreads();
   }
 }
 
-size_t rhs_w_smem_colw() { return (size_t)(kCW * kXR + kCW * kW_H + 1024) * sizeof(double2); }
-size_t rhs_w_smem_roww() { return (size_t)(4 * kXR + 2048 + 2 * kW_N2) * sizeof(double2); }
-size_t rhs_w_smem_rowinvw() { return (size_t)(4 * kXR + 2048) * sizeof(double2); }
-size_t rhs_w_smem_colinvw() { return (size_t)(kCW * kXR + 1024) * sizeof(double2); }
+template <int CW, bool STAGE>
+static size_t smem_colw() { return (size_t)(CW * kXR + (STAGE ? CW * kW_H : 0) + 1024) * sizeof(double2); }
+template <bool STAGE>
+static size_t smem_roww() { return (size_t)(4 * kXR + 2048 + (STAGE ? 2 * kW_N2 : 0)) * sizeof(double2); }
+static size_t smem_rowinvw() { return (size_t)(4 * kXR + 2048) * sizeof(double2); }
+template <int CW>
+static size_t smem_colinvw() { return (size_t)(CW * kXR + 1024) * sizeof(double2); }
+
+// tuning knobs (AGK_WVAR): 0 = staged 8-warp column CTAs + staged row CTAs (1/SM);
+// 1 = unstaged 4-warp column CTAs and row CTAs (2/SM); 2 = column staged, row unstaged
+static int wvar() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("AGK_WVAR");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
 cudaError_t rhs_w_set_smem_limits() {
-  cudaError_t e = cudaFuncSetAttribute(k_colw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhs_w_smem_colw());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_roww, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhs_w_smem_roww());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_rowinvw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhs_w_smem_rowinvw());
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_colinvw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rhs_w_smem_colinvw());
+  cudaError_t e;
+#define SET(fn, bytes) \
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
+  SET((k_colw<8, true>), (smem_colw<8, true>()));
+  SET((k_colw<4, false>), (smem_colw<4, false>()));
+  SET((k_roww<true>), (smem_roww<true>()));
+  SET((k_roww<false>), (smem_roww<false>()));
+  SET(k_rowinvw, smem_rowinvw());
+  SET((k_colinvw<8>), (smem_colinvw<8>()));
+  SET((k_colinvw<4>), (smem_colinvw<4>()));
+#undef SET
+  return cudaSuccess;
 }
 
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
   RhsArgs a = a0;
-  a.nblk_colfwd = kW_N2 / kCW;
-  int nsm = 148;
+  if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);
+  const int nsm = 148;
+  const int v = wvar();
+  const bool col8 = v != 1, rowstage = v == 0;
+  const int cw = col8 ? 8 : 4;
+  a.nblk_colfwd = kW_N2 / cw;
   k_transpose_n<<<(kW_H / 32) * (kW_N2 / 32), 256, 0, s>>>(a);
   if (mark) mark(mk, K_TRANSPOSE, s);
   for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
-    const int items = (kW_N2 / kCW) * gc;
-    k_colw<<<items < nsm ? items : nsm, kCW * 32, rhs_w_smem_colw(), s>>>(a, g0, gc);
+    const int items = (kW_N2 / cw) * gc;
+    if (col8) {
+      k_colw<8, true><<<items < nsm ? items : nsm, 256, smem_colw<8, true>(), s>>>(a, g0, gc);
+    } else {
+      k_colw<4, false><<<items < 2 * nsm ? items : 2 * nsm, 128, smem_colw<4, false>(), s>>>(a, g0, gc);
+    }
     if (mark) mark(mk, K_COL_FWD, s);
+    if (g0 + gc >= a.rf) {
+      // fork: all column partials exist -> scalars and the non-birth part on the side stream
+      cudaEventRecord(p.ev_fork, s);
+      cudaStreamWaitEvent(p.side, p.ev_fork, 0);
+      k_scalars_w<<<1, 256, 0, p.side>>>(a);
+      k_dvec<<<4 * nsm, 256, 0, p.side>>>(a);
+      cudaEventRecord(p.ev_join, p.side);
+    }
     const int rows = kW_N1 / 2 + 1;
-    k_roww<<<rows < nsm ? rows : nsm, 128, rhs_w_smem_roww(), s>>>(a, g0, gc, g0 == 0);
+    if (rowstage) {
+      k_roww<true><<<rows < nsm ? rows : nsm, 128, smem_roww<true>(), s>>>(a, g0, gc, g0 == 0);
+    } else {
+      k_roww<false><<<rows < 2 * nsm ? rows : 2 * nsm, 128, smem_roww<false>(), s>>>(a, g0, gc, g0 == 0);
+    }
     if (mark) mark(mk, K_ROW, s);
   }
-  k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, rhs_w_smem_rowinvw(), s>>>(a);
+  k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, smem_rowinvw(), s>>>(a);
   if (mark) mark(mk, K_ROW, s);
-  const int grps = kW_N2 / (2 * kCW);
-  k_colinvw<<<grps < nsm ? grps : nsm, kCW * 32, rhs_w_smem_colinvw(), s>>>(a);
+  // join the side stream (scalars + D) before the inverse column pass
+  cudaStreamWaitEvent(s, p.ev_join, 0);
+  if (col8) {
+    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw<8>(), s>>>(a);
+  } else {
+    k_colinvw<4><<<kW_N2 / 8, 128, smem_colinvw<4>(), s>>>(a);
+  }
   if (mark) mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }
