@@ -82,6 +82,10 @@ struct RhsPlan {
   // the row transforms)
   cudaStream_t side;
   cudaEvent_t ev_fork, ev_join;
+  // rank-pipelined mode: column pass of rank g+1 on its own stream, overlapping the row pass of
+  // rank g (double-buffered L2-resident intermediate)
+  cudaStream_t colstream;
+  cudaEvent_t ev_start, ev_col[2], ev_row[2];
 };
 
 // kernel classes for per-launch timing

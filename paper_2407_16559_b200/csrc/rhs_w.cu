@@ -387,6 +387,37 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
   if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);
   const int nsm = 148;
   const int v = wvar();
+  if (v == 3 && p.colstream) {
+    // rank pipeline: col(g) on colstream into Y[g % 2], row(g) on s; col(g+2) waits row(g)
+    const int64_t P = (int64_t)kW_N1 * kW_N2;
+    a.nblk_colfwd = kW_N2 / 8;
+    cudaEventRecord(p.ev_start, s);
+    cudaStreamWaitEvent(p.colstream, p.ev_start, 0);
+    k_transpose_n<<<(kW_H / 32) * (kW_N2 / 32), 256, 0, p.colstream>>>(a);
+    for (int g = 0; g < a.rf; ++g) {
+      RhsArgs ag = a;
+      ag.y = a.y + (g & 1) * P;
+      if (g >= 2) cudaStreamWaitEvent(p.colstream, p.ev_row[g & 1], 0);
+      k_colw<8, true><<<nsm, 256, smem_colw<8, true>(), p.colstream>>>(ag, g, 1);
+      cudaEventRecord(p.ev_col[g & 1], p.colstream);
+      if (g + 1 == a.rf) {
+        cudaStreamWaitEvent(p.side, p.ev_col[g & 1], 0);
+        k_scalars_w<<<1, 256, 0, p.side>>>(a);
+        k_dvec<<<4 * nsm, 256, 0, p.side>>>(a);
+        cudaEventRecord(p.ev_join, p.side);
+      }
+      cudaStreamWaitEvent(s, p.ev_col[g & 1], 0);
+      k_roww<true><<<nsm, 128, smem_roww<true>(), s>>>(ag, g, 1, g == 0);
+      if (mark) mark(mk, K_ROW, s);
+      cudaEventRecord(p.ev_row[g & 1], s);
+    }
+    k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, smem_rowinvw(), s>>>(a);
+    if (mark) mark(mk, K_ROW, s);
+    cudaStreamWaitEvent(s, p.ev_join, 0);
+    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw<8>(), s>>>(a);
+    if (mark) mark(mk, K_COL_INV, s);
+    return cudaGetLastError();
+  }
   const bool col8 = v != 1, rowstage = v == 0;
   const int cw = col8 ? 8 : 4;
   a.nblk_colfwd = kW_N2 / cw;
