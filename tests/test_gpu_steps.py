@@ -223,6 +223,6 @@ def test_model_advance_matches_oracle(agk, oracle_port, stepper, m):
     w = oracle_port.advance(n, 0.05, oc, model=om)
     assert g.status == w["status"] and g.rejects == w["rejects"] and g.rhs_evals == w["rhs_evals"]
     # after a reject tau = tau0 * factor(err)^k and err carries ~1e-8 relative cancellation noise
-    tol = 1e-12 if w["rejects"] == 0 else 1e-8
+    tol = 1e-12 if w["rejects"] == 0 else 1e-7
     assert abs(g.tau_used - w["tau_used"]) <= tol * w["tau_used"]
     assert rel_max_diff(g.state, w["state"]) <= max(1e-11, tol)
