@@ -500,6 +500,12 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
     CK_C(cudaEventCreateWithFlags(&h->plan.ev_fork, cudaEventDisableTiming), "event");
     CK_C(cudaEventCreateWithFlags(&h->plan.ev_join, cudaEventDisableTiming), "event");
     CK_C(cudaStreamCreateWithFlags(&h->plan.colstream, cudaStreamNonBlocking), "col stream");
+    CK_C(dalloc(hp, &h->plan.pipe_counters, 2 * (size_t)h->rf + 1), "alloc counters");
+    {
+      int nsm = 0;
+      CK_C(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, hp->device), "SM count");
+      h->plan.nsm = nsm;
+    }
     CK_C(cudaEventCreateWithFlags(&h->plan.ev_start, cudaEventDisableTiming), "event");
     for (int q = 0; q < 2; ++q) {
       CK_C(cudaEventCreateWithFlags(&h->plan.ev_col[q], cudaEventDisableTiming), "event");

@@ -86,6 +86,9 @@ struct RhsPlan {
   // rank g (double-buffered L2-resident intermediate)
   cudaStream_t colstream;
   cudaEvent_t ev_start, ev_col[2], ev_row[2];
+  // persistent pipelined core: per-rank counters (2 x 16 + 1) and the SM count
+  unsigned* pipe_counters;
+  int nsm;
 };
 
 // kernel classes for per-launch timing

@@ -431,8 +431,6 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   if (g > rf) g = rf;
   const char* fe0 = getenv("AGK_FAST");
   if (L == 21 && !(fe0 && atoi(fe0) == 0) && g > 16) g = 16;  // warp path: <= 16 rank slots
-  if (const char* wv = getenv("AGK_WVAR"))
-    if (L == 21 && atoi(wv) == 3 && g > 2) g = 2;  // rank pipeline: two L2-resident buffers
   p->gsize = g;
   const int ngroups = (rf + g - 1) / g;
   const char* fe = getenv("AGK_FAST");
@@ -441,6 +439,8 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->side = nullptr;
   p->ev_fork = p->ev_join = nullptr;
   p->colstream = nullptr;
+  p->pipe_counters = nullptr;
+  p->nsm = 148;
 }
 
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
