@@ -30,7 +30,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libagk_b200.so")
+LIB_PATH = os.environ.get("AGK_LIB") or os.path.join(_HERE, "libagk_b200.so")  # AGK_LIB: A/B experiments
 
 # enums mirrored from include/agk/agk.h
 AGGREGATION, AGGREGATION_SOURCES, AGGREGATION_SHATTERING = 0, 1, 2
@@ -465,7 +465,7 @@ def run(ws: RhsWorkspace, cfg: SimulationConfig) -> RunReport:
                      rep.total_accepted, rep.total_rejects, rep.wall_seconds)
 
 
-KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv", "transpose")
+KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv", "transpose", "dvec", "row_inv")
 
 
 def eval_rhs_timed(ws: RhsWorkspace, n_dev, out_dev, count: int) -> float:

@@ -496,20 +496,10 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
     double* dvec;
     CK_C(dalloc(hp, &dvec, (size_t)m), "alloc D");
     a.dvec = dvec;
-    CK_C(cudaStreamCreateWithFlags(&h->plan.side, cudaStreamNonBlocking), "side stream");
-    CK_C(cudaEventCreateWithFlags(&h->plan.ev_fork, cudaEventDisableTiming), "event");
-    CK_C(cudaEventCreateWithFlags(&h->plan.ev_join, cudaEventDisableTiming), "event");
-    CK_C(cudaStreamCreateWithFlags(&h->plan.colstream, cudaStreamNonBlocking), "col stream");
-    CK_C(dalloc(hp, &h->plan.pipe_counters, 2 * (size_t)h->rf + 1), "alloc counters");
     {
       int nsm = 0;
       CK_C(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, hp->device), "SM count");
       h->plan.nsm = nsm;
-    }
-    CK_C(cudaEventCreateWithFlags(&h->plan.ev_start, cudaEventDisableTiming), "event");
-    for (int q = 0; q < 2; ++q) {
-      CK_C(cudaEventCreateWithFlags(&h->plan.ev_col[q], cudaEventDisableTiming), "event");
-      CK_C(cudaEventCreateWithFlags(&h->plan.ev_row[q], cudaEventDisableTiming), "event");
     }
     a.uvg = uvg;
     a.ng = ng;
@@ -587,17 +577,6 @@ void agk_rhs_destroy(agk_rhs* h) {
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->rhs_graph) cudaGraphExecDestroy(h->rhs_graph);
   for (void* p : h->allocs) cudaFree(p);
-  if (h->plan.side) cudaStreamDestroy(h->plan.side);
-  if (h->plan.colstream) {
-    cudaStreamDestroy(h->plan.colstream);
-    cudaEventDestroy(h->plan.ev_start);
-    for (int q = 0; q < 2; ++q) {
-      cudaEventDestroy(h->plan.ev_col[q]);
-      cudaEventDestroy(h->plan.ev_row[q]);
-    }
-  }
-  if (h->plan.ev_fork) cudaEventDestroy(h->plan.ev_fork);
-  if (h->plan.ev_join) cudaEventDestroy(h->plan.ev_join);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
   if (h->stream) cudaStreamDestroy(h->stream);

@@ -331,6 +331,32 @@ __device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, cons
   Dft<32, SIGN>::run(v);
 }
 
+// The same transform with the exchange inside an interleaved tile of 1024 rows x 8 chunks (16 B):
+// warp w's entry i lives at chunk w ^ ((i ^ (i >> 5)) & 7) of row i. The XOR swizzle keeps both
+// exchange patterns (i = 32k + lane and i = 32 lane + l) conflict-free, and since each warp owns
+// one chunk per row, eight warps can share one tile without synchronising.
+__device__ __forceinline__ int tile_idx(int i, int w) { return i * 8 + (w ^ ((i ^ (i >> 5)) & 7)); }
+template <int SIGN, bool HALFZERO>
+__device__ __forceinline__ void warp_fft1024_t(double2 (&v)[32], double2* T, int w, const double2* tw, int lane) {
+  if constexpr (HALFZERO) {
+    dft_halfzero<32, SIGN>(v);
+  } else {
+    Dft<32, SIGN>::run(v);
+  }
+#pragma unroll
+  for (int k = 1; k < 32; ++k) {
+    const double2 t = tw[k * 32 + lane];
+    v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[tile_idx(32 * k + lane, w)] = v[k];
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; ++l) v[l] = T[tile_idx(32 * lane + l, w)];
+  Dft<32, SIGN>::run(v);
+}
+
 // W_P^e for the four-step twiddles, e < P, from two short tables:
 // W_P^e = hi[e >> s] * lo[e & (2^s - 1)].
 struct TwoLevel {

@@ -66,7 +66,7 @@ struct RhsArgs {
   double* ng;
   const double2* tw32;     // [k1*32 + l] = W_1024^{l k1}
   const double2* tw2048h;  // [r*32 + l] = W_2048^{l + 32 r}
-  double* dvec;            // m: the non-birth part of S (death, sources, shattering), side stream
+  double* dvec;            // m: the non-birth part of S (death, sources, shattering)
   int dbg;                 // experiment switches (AGK_DBG), 0 in production
 };
 
@@ -78,21 +78,12 @@ struct RhsPlan {
   int n1, n2, c, cp;
   int gsize;     // ranks per group in the four-step path
   int launches;  // kernels per RHS
-  // fast path: side stream + fork/join events (the death / row-sum pass runs concurrently with
-  // the row transforms)
-  cudaStream_t side;
-  cudaEvent_t ev_fork, ev_join;
-  // rank-pipelined mode: column pass of rank g+1 on its own stream, overlapping the row pass of
-  // rank g (double-buffered L2-resident intermediate)
-  cudaStream_t colstream;
-  cudaEvent_t ev_start, ev_col[2], ev_row[2];
-  // persistent pipelined core: per-rank counters (2 x 16 + 1) and the SM count
-  unsigned* pipe_counters;
+  // SM count (grid sizing of the fast path)
   int nsm;
 };
 
 // kernel classes for per-launch timing
-enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4 };
+enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4, K_DVEC = 5, K_ROW_INV = 6 };
 
 // host-side launchers (rhs.cu)
 void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);

@@ -436,10 +436,6 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   const char* fe = getenv("AGK_FAST");
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
   p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 4 : 0);
-  p->side = nullptr;
-  p->ev_fork = p->ev_join = nullptr;
-  p->colstream = nullptr;
-  p->pipe_counters = nullptr;
   p->nsm = 148;
 }
 

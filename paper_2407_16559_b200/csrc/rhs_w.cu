@@ -4,25 +4,27 @@
 // Same algebra as rhs.cu's four-step path (reference rhs.cpp:87-151 birth, 24-46 death,
 // 170-210 shattering), restructured so every 1024-point transform is owned by ONE warp
 // (warp_fft1024: two register radix-32 DFTs around one warp-private shared-memory exchange) —
-// no block-wide barrier inside a transform, 2x fewer shared-memory passes than the radix-16
-// Stockham path:
+// no block-wide barrier inside a transform:
 //   k_transpose_n : n -> column-major grid layout ng (so each column's operands are contiguous)
-//   k_colw        : per (column, rank): z = (U_a n, V_a n) from the column-major UV copy (cp.async
-//                   prefetch of the next rank), 1024-pt forward FFT (upper half zero), four-step
-//                   twiddle, block-cooperative coalesced store of the Y tile; moment partials.
-//   k_roww        : per row pair (k1, N1-k1), 4 warps: radix-2 DIF across two warps per row +
-//                   1024-pt FFTs, conjugate-pair split, w*A*B summed over ranks in registers; then
-//                   the inverse row transform of the Hermitian half-row and the inverse twiddle -> G.
+//   k_colt        : per (column octet, rank): z = (U_a n, V_a n) from the column-major UV copy
+//                   (cp.async prefetch of the next item), 1024-pt forward FFT (upper half zero)
+//                   exchanging inside one swizzled shared tile, four-step twiddle, full-line
+//                   store of the tile into the even/odd-permuted Y rows; moment partials.
+//   k_rowd        : per row pair (k1, N1-k1) x rank: 1024-pt FFTs of the even and odd samples,
+//                   the decimation-in-time radix-2 stage fused into the conjugate-pair split,
+//                   w*A*B summed over ranks in registers. Two independent 4-warp halves per CTA.
+//   k_rowinvw     : inverse row transform of the Hermitian half-rows, inverse twiddle -> G.
 //   k_colinvw     : per column pair, 1024-pt inverse FFT of G_a + i G_b (two real outputs),
-//                   epilogue (birth/death/sources/shattering) block-cooperative and coalesced.
+//                   epilogue birth + D, where D (death/sources/shattering) came from k_dvec.
 #include "rhs_common.cuh"
 
 namespace agk {
 
 constexpr int kW_N1 = 1024, kW_N2 = 2048, kW_H = kW_N1 / 2;
-constexpr int kCW = 8;            // warps (columns) per column-kernel CTA
-constexpr int kXR = kXS + 1;      // region stride (double2): successive regions on different banks
-
+// Region stride (double2) of the per-warp exchange / output regions: = 4 (mod 8) so that two
+// regions read at the same offset by neighbouring lanes sit on different 16-byte bank groups
+// (the tile store of k_colh and the split product of k_rowh both read region pairs that way).
+constexpr int kXR = kXS + 4;
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -30,6 +32,9 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 32x32 tiles.
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 32x32 tiles.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   if (a.skip && *a.skip) return;
@@ -51,65 +56,60 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   }
 }
 
-// EOI: the group is columns {4 grp + j} and {1024 + 4 grp + j}, j < 4, and the tile store applies
-// the first radix-2 DIF stage of the row transform, E[j] = y[j] + y[j + 1024] and
-// O[j] = (y[j] - y[j + 1024]) W_2048^j, written interleaved in 64-byte chunks so each row of the
-// tile is one full 128-byte line: Y row k1 = [E 0..3 | O 0..3 | E 4..7 | O 4..7 | ...]. The row
-// kernel's warps then load their 1024-point half-row directly and run no combine pass.
-template <int kCW, bool STAGE, bool EOI = false>
-__global__ void __launch_bounds__(kCW * 32, STAGE ? 1 : 2) k_colw(RhsArgs a, int g0, int gcount) {
+// Y layout (per rank, [k1][slot], 2048 slots per row): the row transform's first radix-2 stage
+// is decimation in time, so each row is stored even/odd-permuted, slot(n2) = (n2 & 1) * 1024 +
+// (n2 >> 1): a row-pass warp then loads its 1024 even or odd samples as contiguous full lines.
+//
+// Column pass: a CTA item is (column octet o, rank): the 8 columns n2 = 16 (o >> 1) + 2 w + (o & 1)
+// (warp w), whose outputs are the 8 consecutive slots (o & 1) * 1024 + 8 (o >> 1) + w of every
+// row. Each warp's 1024-point transform exchanges through, and leaves its twiddled output in, its
+// own chunk of one swizzled 1024 x 8 tile; the CTA then writes the tile back as full 128-byte row
+// lines (4 lines per warp store). Items are rank-minor, so n is reloaded only per octet.
+__global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) {
   extern __shared__ double2 smem[];
-  double2* X = smem;                       // kCW exchange / output regions
-  double2* S = X + kCW * kXR;              // kCW staging regions (512 x (U,V)), STAGE only
-  double2* tw = S + (STAGE ? kCW * kW_H : 0);  // W_1024^{l k1}, [k1][l]
-  __shared__ double red[kCW][4];
-  __shared__ double2 tk[kCW][32];  // four-step factors W_P^{32 n2 k} of the warp's column
+  double2* T = smem;               // 1024 x 8 tile: exchange + output (tile_idx)
+  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
+  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
+  __shared__ double red[8][4];
+  __shared__ double2 tk[8][32];    // four-step factors W_P^{32 n2 k} of the warp's column
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int ngroups = kW_N2 / kCW;
-  // persistent over (column group, rank) items, rank-minor so n is reloaded only per group
-  const int items = ngroups * gcount;
+  const int items = (kW_N2 / 8) * gcount;
   const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
   const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
   for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
   double2* Sw = S + w * kW_H;
-  double2* Xw = X + w * kXR;
+  auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * w + (o & 1); };
   auto prefetch = [&](int item) {
-    if constexpr (STAGE) {
-      const int grp = item / gcount, ub = g0 + item % gcount;
-      const int n2 = EOI ? (w < 4 ? 4 * grp + w : kW_N2 / 2 + 4 * grp + w - 4) : grp * kCW + w;
-      const double2* src = a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
+    const int o = item / gcount, ub = g0 + item % gcount;
+    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
 #pragma unroll
-      for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
-      cp_async_commit();
-    }
+    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
+    cp_async_commit();
   };
   if (it0 < it1) prefetch(it0);
   __syncthreads();
   double nl[16];
   double2 base = czero();
-  int cur_grp = -1;
+  int cur_o = -1;
   const int64_t P = (int64_t)kW_N1 * kW_N2;
   for (int item = it0; item < it1; ++item) {
-    const int grp = item / gcount, g = item % gcount, ub = g0 + g;
-    const int n2 = EOI ? (w < 4 ? 4 * grp + w : kW_N2 / 2 + 4 * grp + w - 4) : grp * kCW + w;
-    if (grp != cur_grp) {
-      cur_grp = grp;
+    const int o = item / gcount, g = item % gcount, ub = g0 + g;
+    const int n2 = col_of(o);
+    if (o != cur_o) {
+      cur_o = o;
 #pragma unroll
       for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
       base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
       tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
     }
-    if constexpr (STAGE) {
-      cp_async_wait_all();
-      __syncwarp();
-    }
-    const double2* uvsrc = STAGE ? Sw : a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
+    cp_async_wait_all();
+    __syncwarp();
     double2 v[32];
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const double2 uv = uvsrc[lane + 32 * r];
+      const double2 uv = Sw[lane + 32 * r];
       const double x = uv.x * nl[r], y = uv.y * nl[r];
       v[r] = make_double2(x, y);
       const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
@@ -125,11 +125,11 @@ __global__ void __launch_bounds__(kCW * 32, STAGE ? 1 : 2) k_colw(RhsArgs a, int
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
-    if (!(a.dbg & 1)) warp_fft1024<-1, true>(v, Xw, tw, lane);
+    if (!(a.dbg & 1)) warp_fft1024_t<-1, true>(v, T, w, tw, lane);
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = cmul(v[k], cmul(base, tk[w][k]));
+    for (int k = 0; k < 32; ++k) T[tile_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
@@ -141,231 +141,202 @@ __global__ void __launch_bounds__(kCW * 32, STAGE ? 1 : 2) k_colw(RhsArgs a, int
       red[w][3] = s3;
     }
     __syncthreads();
-    // coalesced store of the tile: rows k1c, kCW consecutive columns
-    double2* __restrict__ yg = a.y + (int64_t)g * P + (int64_t)grp * kCW;
-    if constexpr (EOI) {
-      static_assert(!EOI || kCW == 8, "EOI groups are 4 + 4 columns");
-      const int j = tid & 3;
-      const double2 wj = a.tw2048h[4 * grp + j];  // W_2048^{4 grp + j}
-      if (!(a.dbg & 2)) {
-#pragma unroll 4
-        for (int it = 0; it < kW_N1 / 64; ++it) {
-          const int k1c = (tid >> 2) + 64 * it;
-          const double2 lo = X[j * kXR + k1c], hi = X[(4 + j) * kXR + k1c];
-          yg[(int64_t)k1c * kW_N2 + j] = cadd(lo, hi);
-          yg[(int64_t)k1c * kW_N2 + 4 + j] = cmul(csub(lo, hi), wj);
-        }
-      }
-    } else if (!(a.dbg & 2)) {
-      for (int idx = tid; idx < kW_N1 * kCW; idx += blockDim.x) {
-        const int k1c = idx / kCW, ww = idx % kCW;
-        yg[(int64_t)k1c * kW_N2 + ww] = X[ww * kXR + k1c];
+    if (!(a.dbg & 2)) {
+      double2* __restrict__ yg = a.y + (int64_t)g * P + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+#pragma unroll 8
+      for (int it = 0; it < kW_N1 / 32; ++it) {
+        const int idx = tid + 256 * it, row = idx >> 3, c = idx & 7;
+        yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
       }
     }
     if (tid < 4) {
       double t = 0.0;
-      for (int q = 0; q < kCW; ++q) t += red[q][tid];
-      a.partials[((int64_t)ub * a.nblk_colfwd + grp) * 4 + tid] = t;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += red[q][tid];
+      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
     }
     __syncthreads();
   }
 }
 
-// row pair (k1, N1-k1): warps (rho, h): rho = row, h = output parity of the radix-2 DIF split.
-// One CTA of 4 warps per SM; the next rank's two rows are staged by cp.async while this rank's
-// transforms run (the warp FFT keeps ~90% of its throughput at one warp per SMSP).
-template <bool STAGE>
-__global__ void __launch_bounds__(128, STAGE ? 1 : 2) k_roww(RhsArgs a, int g0, int gcount, int first) {
+// Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
+// row pair (k1, N1-k1) at a time with warps (rho, h) = (row, even/odd samples). Per rank a warp
+// loads its 1024 samples (contiguous: the permuted Y layout) and transforms them to E (h = 0) or
+// O (h = 1); the half then forms X[q'] = E + W_2048^q' O, X[q' + 1024] = E - W_2048^q' O of both
+// rows, the conjugate-pair split and w*A*B, accumulated over ranks in registers.
+// Launched with 2 row pairs per half (grid = ceil(513 / 4) = 129 CTAs at N1 = 1024) so the SMs
+// left over run the non-birth part D concurrently (k_dvec, programmatic dependent launch).
+template <bool PREF>
+__global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, int first) {
   extern __shared__ double2 smem[];
-  double2* X = smem;               // 4 regions
-  double2* tw = X + 4 * kXR;       // W_1024^{l k1}, [k1][l]
-  double2* twh = tw + 1024;        // W_2048^{l + 32 r}, [r][l]
-  double2* St = twh + 1024;        // staging: 2 rows x 2048
+  double2* X = smem;               // 8 regions: per half E1, O1 (row k1), E2, O2 (row N1-k1)
+  double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
+  double2* twh = tw + 1024;        // W_2048^j, j < 1024
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.skip && *a.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, rho = w >> 1, h = w & 1;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
+            h = hw & 1, ht = tid & 127, bar = 1 + hf;
   const int n1 = a.n1;
-  const int P = kW_N1 * kW_N2;
+  const int64_t P = (int64_t)kW_N1 * kW_N2;
   const int nrows = n1 / 2 + 1;
-  // items: (row pair k1, rank g), rank-minor; a CTA owns whole row pairs (acc in registers)
-  auto prefetch = [&](int k1, int g) {
-    if constexpr (!STAGE) return;
-    if (a.dbg & 64) return;
-    const double2* y0 = a.y + (int64_t)g * P + (int64_t)k1 * kW_N2;
-    const double2* y1 = a.y + (int64_t)g * P + (int64_t)((n1 - k1) & (n1 - 1)) * kW_N2;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int e = tid + 128 * q;
-      cp_async16(St + e, y0 + e);
-      cp_async16(St + kW_N2 + e, y1 + e);
-    }
-    cp_async_commit();
-  };
-  if ((int)blockIdx.x < nrows && gcount > 0) prefetch(blockIdx.x, 0);
   for (int i = tid; i < 1024; i += blockDim.x) {
     tw[i] = __ldg(a.tw32 + i);
     twh[i] = __ldg(a.tw2048h + i);
   }
-  double2* Xw = X + w * kXR;
-  const double2* Sr = St + rho * kW_N2;
-  for (int k1 = blockIdx.x; k1 < nrows; k1 += gridDim.x) {
-    double2 acc[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + tid + 128 * j];
-    for (int g = 0; g < gcount; ++g) {
-      const double wt = a.uniq_weight[g0 + g];
-      if constexpr (STAGE) { if (!(a.dbg & 64)) cp_async_wait_all(); }
-      __syncthreads();  // staged rows visible; previous split done with X
-      double2 v[32];
-      const double2* src = STAGE ? Sr : a.y + (int64_t)g * P + (int64_t)(rho == 0 ? k1 : (n1 - k1) & (n1 - 1)) * kW_N2;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const double2 lo = src[lane + 32 * r], hi = src[1024 + lane + 32 * r];
-        v[r] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), twh[r * 32 + lane]);
-      }
-      __syncthreads();  // everyone has read the staging buffer
-      if (g + 1 < gcount) {
-        prefetch(k1, g + 1);
-      } else if (k1 + (int)gridDim.x < nrows && gcount > 0) {
-        prefetch(k1 + gridDim.x, 0);
-      }
-      if (!(a.dbg & 16)) warp_fft1024<-1, false>(v, Xw, tw, lane);
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];  // X_row[2(lane + 32k) + h]
-      __syncthreads();
-      if (!(a.dbg & 32))
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int q = tid + 128 * j;
-        const int pq = (k1 == 0) ? ((kW_N2 - q) & (kW_N2 - 1)) : (kW_N2 - 1 - q);
-        const double2 z = X[(q & 1) * kXR + (q >> 1)];
-        const double2 zp = X[(2 + (pq & 1)) * kXR + (pq >> 1)];
-        const double2 pr = split_product(z, zp);
-        acc[j].x += wt * pr.x;
-        acc[j].y += wt * pr.y;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 16; ++j) a.acc[(int64_t)k1 * kW_N2 + tid + 128 * j] = acc[j];
-  }
-}
-
-// W_64^r = exp(-2 pi i r / 64) for r < 32, a compile-time constant after unrolling
-__device__ __forceinline__ double2 w64(int r) {
-  constexpr double c[17] = {1.0,
-                            0.99518472667219688624,
-                            0.98078528040323044913,
-                            0.95694033573220886494,
-                            0.92387953251128675613,
-                            0.88192126434835502971,
-                            0.83146961230254523708,
-                            0.77301045336273696081,
-                            0.70710678118654752440,
-                            0.63439328416364549822,
-                            0.55557023301960222474,
-                            0.47139673682599764856,
-                            0.38268343236508977173,
-                            0.29028467725446236764,
-                            0.19509032201612826785,
-                            0.09801714032956060199,
-                            0.0};
-  // cos(2 pi r / 64) and sin(2 pi r / 64) = cos(2 pi (16 - r) / 64)
-  const double cs = r <= 16 ? c[r] : -c[32 - r];
-  const double sn = r <= 16 ? c[16 - r] : c[r - 16];
-  return make_double2(cs, -sn);
-}
-
-// Row kernel: 8 warps = two independent halves (named barriers), each half owning one row pair
-// (k1, N1-k1) at a time with warps (rho, h) = (row, output parity of the radix-2 DIF split).
-// Every warp loads its own quarter of the row pair straight from global memory -- lo[j], hi[j]
-// for 512 consecutive j -- forms E[j] = lo + hi and O[j] = (lo - hi) W_2048^j in registers and
-// swaps the half its partner warp needs through its shared-memory region, so global loads are
-// full-line coalesced, nothing is staged, and each 2048-point row costs two 1024-point warp FFTs.
-// The two halves drift out of phase: one half's loads overlap the other half's transforms. The
-// conjugate-pair split and w*A*B accumulate in registers over all ranks.
-// Launched with 2 row pairs per half (grid = ceil(513 / 4) = 129 CTAs at N1 = 1024) so the SMs
-// left over run the non-birth part D concurrently (k_dvec, programmatic dependent launch).
-template <bool EOI>
-__global__ void __launch_bounds__(256, 1) k_rown(RhsArgs a, int g0, int gcount, int first) {
-  extern __shared__ double2 smem[];
-  double2* X = smem;               // 8 regions: per half, row k1 (h = 0, 1) and row N1-k1 (h = 0, 1)
-  double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (a.skip && *a.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
-            h = hw & 1, ht = tid & 127;
-  const int n1 = a.n1;
-  const int64_t P = (int64_t)kW_N1 * kW_N2;
-  const int nrows = n1 / 2 + 1;
-  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
-  const double2 wl = tw_p<-1>(a.twp, (uint32_t)(lane * (P / kW_N2)));  // W_2048^lane
   __syncthreads();
-  double2* Xh = X + hf * 4 * kXR;
+  const double2* Xh = X + hf * 4 * kXR;
   double2* Xw = X + w * kXR;
-  const double2* Xp = X + (w ^ 1) * kXR;
-  const int bar = 1 + hf, pbar = 3 + (w >> 1);
+  double2 v[32];
   for (int k1 = 2 * blockIdx.x + hf; k1 < nrows; k1 += 2 * gridDim.x) {
     const int row = rho == 0 ? k1 : (n1 - k1) & (n1 - 1);
-    const double2* rsrc = a.y + (int64_t)g0 * P + (int64_t)row * kW_N2 + h * (kW_N2 / 4);
+    const double2* __restrict__ rsrc = a.y + (int64_t)row * kW_N2 + h * (kW_N2 / 2);
     double2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j];
+    if (PREF && k1 == 2 * (int)blockIdx.x + hf) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = rsrc[lane + 32 * r];
+    }
     for (int g = 0; g < gcount; ++g) {
       const double wt = a.uniq_weight[g0 + g];
       const double2* __restrict__ src = rsrc + (int64_t)g * P;
-      double2 v[32];
-      if constexpr (EOI) {
-        // element e of E (h = 0) / O (h = 1) sits at (e / 4) * 8 + 4 h + e % 4 of the row
-        const double2* __restrict__ sh = src - h * (kW_N2 / 4) + 4 * h + (lane & 3) + 2 * (lane & ~3);
+      if (PREF) {
+      } else if (!(a.dbg & 64)) {
 #pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = sh[64 * r];
+        for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       } else {
-        // j = 512 h + lane + 32 r: E -> FFT slot (j mod 1024) / 32 of warp 0, O -> of warp 1
-        if (h == 0) {
-  #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const double2 lo = src[lane + 32 * r], hi = src[kW_N2 / 2 + lane + 32 * r];
-            v[r] = cadd(lo, hi);
-            Xw[32 * r + lane] = cmul(csub(lo, hi), cmul(wl, w64(r)));
-          }
-        } else {
-  #pragma unroll
-          for (int r = 0; r < 16; ++r) {
-            const double2 lo = src[lane + 32 * r], hi = src[kW_N2 / 2 + lane + 32 * r];
-            v[16 + r] = cmul(csub(lo, hi), cmul(wl, w64(16 + r)));
-            Xw[32 * r + lane] = cadd(lo, hi);
-          }
-        }
-        asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
-        if (h == 0) {
-  #pragma unroll
-          for (int r = 0; r < 16; ++r) v[16 + r] = Xp[32 * r + lane];
-        } else {
-  #pragma unroll
-          for (int r = 0; r < 16; ++r) v[r] = Xp[32 * r + lane];
-        }
-        asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = make_double2(r, lane);
       }
       if (!(a.dbg & 16)) warp_fft1024<-1, false>(v, Xw, tw, lane);
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];  // X_row[2(lane + 32k) + h]
-      asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+      for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
+      if (PREF) {
+        // next item's samples into the idle transform registers (in flight during the split)
+        const int nk = g + 1 < gcount ? k1 : k1 + 2 * (int)gridDim.x;
+        const int ng = g + 1 < gcount ? g + 1 : 0;
+        if (nk < nrows) {
+          const int nrow = rho == 0 ? nk : (n1 - nk) & (n1 - 1);
+          const double2* __restrict__ ns = a.y + (int64_t)ng * P + (int64_t)nrow * kW_N2 + h * (kW_N2 / 2);
+#pragma unroll
+          for (int r = 0; r < 32; ++r) v[r] = ns[lane + 32 * r];
+        }
+      }
+      bar_sync(bar, 128);
       if (!(a.dbg & 32))
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int q = ht + 128 * j;
-        const int pq = (k1 == 0) ? ((kW_N2 - q) & (kW_N2 - 1)) : (kW_N2 - 1 - q);
-        const double2 z = Xh[(q & 1) * kXR + (q >> 1)];
-        const double2 zp = Xh[(2 + (pq & 1)) * kXR + (pq >> 1)];
-        const double2 pr = split_product(z, zp);
-        acc[j].x += wt * pr.x;
-        acc[j].y += wt * pr.y;
+      for (int j = 0; j < 8; ++j) {
+        const int qp = ht + 128 * j;
+        // partner bins of q' and q' + 1024 in row N1-k1 (row 0 pairs with itself at N2 - q)
+        const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
+        const double sa = (k1 == 0 && qp == 0) ? 1.0 : -1.0;
+        const double2 e1 = Xh[qp], o1 = Xh[kXR + qp];
+        const double2 e2 = Xh[2 * kXR + m], o2 = Xh[3 * kXR + m];
+        const double2 t1 = cmul(o1, twh[qp]), t2 = cmul(o2, twh[m]);
+        const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
+        const double2 pa = make_double2(e2.x + sa * t2.x, e2.y + sa * t2.y);
+        const double2 pb = make_double2(e2.x - sa * t2.x, e2.y - sa * t2.y);
+        const double2 ra = split_product(xa, pa), rb = split_product(xb, pb);
+        acc[j].x += wt * ra.x;
+        acc[j].y += wt * ra.y;
+        acc[j + 8].x += wt * rb.x;
+        acc[j + 8].y += wt * rb.y;
       }
-      asm volatile("bar.sync %0, 128;" ::"r"(bar) : "memory");
+      bar_sync(bar, 128);
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j) a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j] = acc[j];
+  }
+}
+
+// Row pass, variant 2: one row pair (k1, N1-k1) per CTA at a time, TWO ranks per step (warps
+// 0-3 rank g, warps 4-7 rank g+1; warp (rho, h) = (row, even/odd samples)). Each of the 256
+// threads then owns 4 bins q' (8 accumulators: q' and q' + 1024), which keeps the register
+// accumulators beside the transform without spilling; the next step's samples are loaded into
+// the (idle) transform registers before the split, so the loads overlap the split.
+__global__ void __launch_bounds__(256, 1) k_rowd2(RhsArgs a, int g0, int gcount, int first) {
+  extern __shared__ double2 smem[];
+  double2* X = smem;               // 8 regions: [rank slot][E1, O1, E2, O2]
+  double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
+  double2* twh = tw + 1024;        // W_2048^j, j < 1024
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gi = w >> 2, hw = w & 3, rho = hw >> 1, h = hw & 1;
+  const int n1 = a.n1;
+  const int64_t P = (int64_t)kW_N1 * kW_N2;
+  const int nrows = n1 / 2 + 1;
+  for (int i = tid; i < 1024; i += blockDim.x) {
+    tw[i] = __ldg(a.tw32 + i);
+    twh[i] = __ldg(a.tw2048h + i);
+  }
+  __syncthreads();
+  double2* Xw = X + w * kXR;
+  const bool pref = !(a.dbg & 128);
+  auto load = [&](double2 (&v)[32], int kk, int g) {
+    const int row = rho == 0 ? kk : (n1 - kk) & (n1 - 1);
+    const double2* __restrict__ src = a.y + (int64_t)g * P + (int64_t)row * kW_N2 + h * (kW_N2 / 2);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
+  };
+  int k1 = blockIdx.x;
+  if (k1 >= nrows) return;
+  double2 v[32];
+  if (gi < gcount) load(v, k1, gi);
+  for (; k1 < nrows; k1 += gridDim.x) {
+    double2 acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = tid + 256 * (j & 3) + 1024 * (j >> 2);
+      acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + q];
+    }
+    for (int g = 0; g < gcount; g += 2) {
+      const bool act = g + gi < gcount;
+      if (!pref && act) load(v, k1, g + gi);
+      if (act) {
+        warp_fft1024<-1, false>(v, Xw, tw, lane);
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
+      }
+      if (pref) {
+        if (g + 2 + gi < gcount) {
+          load(v, k1, g + 2 + gi);
+        } else if (k1 + (int)gridDim.x < nrows && gi < gcount) {
+          load(v, k1 + gridDim.x, gi);
+        }
+      }
+      __syncthreads();
+      const int nr = gcount - g < 2 ? gcount - g : 2;
+      for (int s = 0; s < nr; ++s) {
+        const double wt = a.uniq_weight[g0 + g + s];
+        const double2* Xs = X + 4 * s * kXR;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int qp = tid + 256 * j;
+          // partner bins of q' and q' + 1024 in row N1-k1 (row 0 pairs with itself at N2 - q)
+          const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
+          const double sa = (k1 == 0 && qp == 0) ? 1.0 : -1.0;
+          const double2 e1 = Xs[qp], o1 = Xs[kXR + qp];
+          const double2 e2 = Xs[2 * kXR + m], o2 = Xs[3 * kXR + m];
+          const double2 t1 = cmul(o1, twh[qp]), t2 = cmul(o2, twh[m]);
+          const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
+          const double2 pa = make_double2(e2.x + sa * t2.x, e2.y + sa * t2.y);
+          const double2 pb = make_double2(e2.x - sa * t2.x, e2.y - sa * t2.y);
+          const double2 ra = split_product(xa, pa), rb = split_product(xb, pb);
+          acc[j].x += wt * ra.x;
+          acc[j].y += wt * ra.y;
+          acc[j + 4].x += wt * rb.x;
+          acc[j + 4].y += wt * rb.y;
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = tid + 256 * (j & 3) + 1024 * (j >> 2);
+      a.acc[(int64_t)k1 * kW_N2 + q] = acc[j];
+    }
   }
 }
 
@@ -425,7 +396,7 @@ __global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
 
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
 // (rhs.cpp:24-46, 162-168, 170-210, 227-229). A pure stream over U (R x M) at full occupancy;
-// it runs on the side stream while the row transforms run.
+// it runs on the SMs the last row launch leaves free, beside the row transforms.
 __global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
   if (!(a.skip && *a.skip)) {
     const double* __restrict__ n = a.n.get();
@@ -543,381 +514,81 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Rank-pipelined persistent RHS core (one launch per RHS, one CTA of 8 warps per SM, co-resident
-// by cooperative launch). Every CTA walks the same phase sequence
-//     col(0) | col(1) row(0) | col(2) row(1) | ... | row(R-1) + D slice
-// doing its static share of each phase: column groups [b*256/nb, (b+1)*256/nb) and row pairs
-// [b*513/nb, (b+1)*513/nb). Cross-CTA order comes from per-rank counters instead of launches or
-// grid barriers: row(g) waits until every CTA finished col(g); col(g) overwrites the buffer of
-// rank g-2 only after every CTA finished row(g-2). The per-rank intermediate is therefore double-
-// buffered (2 x 32 MiB) and stays in L2; the spectral accumulator (16 MiB) is read-modify-written
-// in L2 per rank. A CTA that finishes a phase early runs ahead into the next one, which absorbs the
-// 256/148 and 513/148 quantisation that per-rank launches pay.
-struct PipeSync {
-  unsigned* col_done;  // [R]
-  unsigned* row_done;  // [R]
-  unsigned* scal_ready;
-};
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void wait_count(const unsigned* c, unsigned target) {
-  if (threadIdx.x == 0) {
-    unsigned v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
-      if (v >= target) break;
-      __nanosleep(200);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ void signal_count(unsigned* c) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(c, 1u);
-  }
-}
-
-__global__ void __launch_bounds__(256, 1) k_pipe(RhsArgs a, PipeSync ps) {
-  extern __shared__ double2 smem[];
-  double2* X = smem;               // 8 exchange / tile regions
-  double2* S = X + 8 * kXR;        // 8 column staging regions (512 x (U,V))
-  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
-  __shared__ double red[8][4];
-  __shared__ double2 tk[8][32];
-  if (a.skip && *a.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int nb = gridDim.x, b = blockIdx.x;
-  const int R = a.rf;
-  const int64_t P = (int64_t)kW_N1 * kW_N2;
-  const int ngroups = kW_N2 / 8, nrows = kW_N1 / 2 + 1;
-  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
-  const double2 wl = tw_p<-1>(a.twp, (uint32_t)(lane * 1024));  // W_2048^lane = W_P^{1024 lane}
-  __syncthreads();
-  const int gb0 = b * ngroups / nb, gb1 = (b + 1) * ngroups / nb;
-  const int pb0 = b * nrows / nb, pb1 = (b + 1) * nrows / nb;
-  double2* Xw = X + w * kXR;
-  double2* Sw = S + w * kW_H;
-
-  auto col_phase = [&](int g) {
-    const int ub = g;
-    double2* yg = a.y + (int64_t)(g & 1) * P;
-    auto prefetch = [&](int grp) {
-      const int n2 = grp * 8 + w;
-      const double2* src = a.uvg + ((int64_t)ub * kW_N2 + n2) * kW_H;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
-      cp_async_commit();
-    };
-    if (gb0 < gb1) prefetch(gb0);
-    for (int grp = gb0; grp < gb1; ++grp) {
-      const int n2 = grp * 8 + w;
-      double nl[16];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
-      const double2 base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
-      tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
-      cp_async_wait_all();
-      __syncwarp();
-      double2 v[32];
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const double2 uv = Sw[lane + 32 * r];
-        const double x = uv.x * nl[r], y = uv.y * nl[r];
-        v[r] = make_double2(x, y);
-        const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;
-        if (i >= 1) {
-          const double sz = (double)(i + 1);
-          s0 += x;
-          s1 += sz * x;
-          s2 += y;
-          s3 += sz * y;
-        }
-      }
-#pragma unroll
-      for (int r = 16; r < 32; ++r) v[r] = czero();
-      __syncwarp();
-      if (grp + 1 < gb1) prefetch(grp + 1);
-      warp_fft1024<-1, true>(v, Xw, tw, lane);
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = cmul(v[k], cmul(base, tk[w][k]));
-      s0 = warp_sum(s0);
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
-      s3 = warp_sum(s3);
-      if (lane == 0) {
-        red[w][0] = s0;
-        red[w][1] = s1;
-        red[w][2] = s2;
-        red[w][3] = s3;
-      }
-      __syncthreads();
-      double2* __restrict__ yt = yg + (int64_t)grp * 8;
-      for (int idx = tid; idx < kW_N1 * 8; idx += blockDim.x) {
-        const int k1c = idx >> 3, ww = idx & 7;
-        yt[(int64_t)k1c * kW_N2 + ww] = X[ww * kXR + k1c];
-      }
-      if (tid < 4) {
-        double t = 0.0;
-        for (int q = 0; q < 8; ++q) t += red[q][tid];
-        a.partials[((int64_t)ub * ngroups + grp) * 4 + tid] = t;
-      }
-      __syncthreads();
-    }
-  };
-
-  // two row pairs at a time: warps 0-3 pair p, warps 4-7 pair p+1; each half syncs on its own
-  // named barrier. acc (16 complex per thread) is read-modify-written in L2 per rank.
-  auto row_phase = [&](int g) {
-    const double wt = a.uniq_weight[g];
-    const double2* yg = a.y + (int64_t)(g & 1) * P;
-    const int half = w >> 2, hw = w & 3, rho = hw >> 1, h = hw & 1, ht = tid & 127;
-    double2* Xh = X + half * 4 * kXR;
-    for (int p0 = pb0; p0 < pb1; p0 += 2) {
-      const int k1 = p0 + half;
-      const bool active = k1 < pb1;
-      if (active) {
-        const int row = rho == 0 ? k1 : (kW_N1 - k1) & (kW_N1 - 1);
-        const double2* __restrict__ src = yg + (int64_t)row * kW_N2;
-        double2 v[32];
-#pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
-#pragma unroll
-        for (int r = 0; r < 32; ++r) {
-          const double2 hi = src[1024 + lane + 32 * r];
-          v[r] = h == 0 ? cadd(v[r], hi) : cmul(csub(v[r], hi), cmul(wl, w64(r)));
-        }
-        warp_fft1024<-1, false>(v, X + w * kXR, tw, lane);
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < 32; ++k) X[w * kXR + lane + 32 * k] = v[k];
-      }
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
-      if (active) {
-        double2* accr = a.acc + (int64_t)k1 * kW_N2;
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          const int q = ht + 128 * j;
-          const int pq = (k1 == 0) ? ((kW_N2 - q) & (kW_N2 - 1)) : (kW_N2 - 1 - q);
-          const double2 z = Xh[(q & 1) * kXR + (q >> 1)];
-          const double2 zp = Xh[(2 + (pq & 1)) * kXR + (pq >> 1)];
-          const double2 pr = split_product(z, zp);
-          double2 acc = g == 0 ? czero() : accr[q];
-          acc.x += wt * pr.x;
-          acc.y += wt * pr.y;
-          accr[q] = acc;
-        }
-      }
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + half) : "memory");
-    }
-  };
-
-  const bool tm = (a.dbg & 128) != 0;
-  unsigned long long tacc[4] = {0, 0, 0, 0}, t0 = tm ? gtime() : 0, tl = t0;
-  auto lap = [&](int k) {
-    if (tm) {
-      const unsigned long long t = gtime();
-      tacc[k] += t - tl;
-      tl = t;
-    }
-  };
-  for (int step = 0; step <= R; ++step) {
-    if (step < R) {
-      if (step >= 2) wait_count(ps.row_done + step - 2, nb);  // buffer (step & 1) free again
-      lap(0);
-      if (!(a.dbg & 256)) col_phase(step);
-      signal_count(ps.col_done + step);
-      lap(1);
-    }
-    if (step >= 1) {
-      wait_count(ps.col_done + step - 1, nb);
-      lap(2);
-      if (!(a.dbg & 512)) row_phase(step - 1);
-      signal_count(ps.row_done + step - 1);
-      lap(3);
-    }
-  }
-  if (tm && tid == 0 && (b % 16 == 0 || b == nb - 1))
-    printf("pipe cta %d: total %.1f us  waitcol %.1f col %.1f waitrow %.1f row %.1f  (groups %d pairs %d)\n", b,
-           1e-3 * (tl - t0), 1e-3 * tacc[0], 1e-3 * tacc[1], 1e-3 * tacc[2], 1e-3 * tacc[3], gb1 - gb0, pb1 - pb0);
-  // scalars (one CTA) and this CTA's slice of the non-birth part D
-  if (b == 0) {
-    wait_count(ps.col_done + R - 1, nb);
-    double* tot = a.scalars + a.r + 2;
-    reduce_partials(a, a.nblk_colfwd, tot);
-    __syncthreads();
-    if (tid == 0) {
-      finalize_scalars(a, tot, a.n.get()[0]);
-      __threadfence();
-      atomicAdd(ps.scal_ready, 1u);
-    }
-  }
-  wait_count(ps.scal_ready, 1);
-  const double* __restrict__ n = a.n.get();
-  RhsArgs bb = a;
-  bb.flags = a.flags & ~T_BIRTH;
-  const int64_t s0 = (int64_t)b * a.m / nb, s1 = (int64_t)(b + 1) * a.m / nb;
-  for (int64_t s = s0 + tid; s < s1; s += blockDim.x) a.dvec[s] = s == 0 ? epilogue0(bb, n) : epilogue(bb, n, s, 0.0);
-}
-
-static size_t smem_pipe() { return (size_t)(8 * kXR + 8 * kW_H + 1024) * sizeof(double2); }
-
-template <int CW, bool STAGE>
-static size_t smem_colw() { return (size_t)(CW * kXR + (STAGE ? CW * kW_H : 0) + 1024) * sizeof(double2); }
-template <bool STAGE>
-static size_t smem_roww() { return (size_t)(4 * kXR + 2048 + (STAGE ? 2 * kW_N2 : 0)) * sizeof(double2); }
-static size_t smem_rown() { return (size_t)(8 * kXR + 1024) * sizeof(double2); }
+static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
+static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
 static size_t smem_rowinvw() { return (size_t)(4 * kXR + 2048) * sizeof(double2); }
-template <int CW>
 static size_t smem_colinvw() {
+  constexpr int CW = 8;
   const size_t tile = (size_t)(kW_N1 / 2 + 1) * (2 * CW + 1);
   return ((tile > (size_t)CW * kXR ? tile : (size_t)CW * kXR) + 1024 + (size_t)kW_H * CW) * sizeof(double2);
-}
-
-// tuning knobs (AGK_WVAR): 8 (default) = interleaved E/O column tiles + direct-load row kernel
-// with D beside it; 7 = natural layout, direct-load row kernel with in-register radix-2;
-// 0/5 = natural layout, staged row CTAs; 1 = unstaged 4-warp CTAs; 2 = row unstaged;
-// 6 = rank-pipelined persistent kernel (experimental)
-static int wvar() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("AGK_WVAR");
-    v = e ? atoi(e) : 8;
-  }
-  return v;
 }
 
 cudaError_t rhs_w_set_smem_limits() {
   cudaError_t e;
 #define SET(fn, bytes) \
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
-  SET((k_colw<8, true>), (smem_colw<8, true>()));
-  SET((k_colw<4, false>), (smem_colw<4, false>()));
-  SET((k_roww<true>), (smem_roww<true>()));
-  SET((k_roww<false>), (smem_roww<false>()));
+  SET(k_colt, smem_colt());
+  SET(k_rowd<false>, smem_rowd());
+  SET(k_rowd<true>, smem_rowd());
+  SET(k_rowd2, smem_rowd());
   SET(k_rowinvw, smem_rowinvw());
-  SET(k_rown<false>, smem_rown());
-  SET(k_rown<true>, smem_rown());
-  SET((k_colw<8, true, true>), (smem_colw<8, true>()));
-  SET(k_pipe, smem_pipe());
-  SET((k_colinvw<8>), (smem_colinvw<8>()));
-  SET((k_colinvw<4>), (smem_colinvw<4>()));
+  SET(k_colinvw<8>, smem_colinvw());
 #undef SET
   return cudaSuccess;
 }
 
+// One RHS: transpose | per rank group: column pass, row pass | scalars before the last row pass,
+// D beside it | inverse row pass | inverse column pass with the epilogue. 7 launches for <= 16
+// unique ranks (the plan's `launches`).
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
   RhsArgs a = a0;
-  if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);
-  const int nsm = 148;
-  const int v = wvar();
-  if (v == 6 && p.pipe_counters) {
-    // rank-pipelined persistent core (experimental): one cooperative launch for all ranks
-    a.nblk_colfwd = kW_N2 / 8;
-    k_transpose_n<<<(kW_H / 32) * (kW_N2 / 32), 256, 0, s>>>(a);
-    if (mark) mark(mk, K_TRANSPOSE, s);
-    cudaMemsetAsync(p.pipe_counters, 0, (2 * (size_t)a.rf + 1) * sizeof(unsigned), s);
-    PipeSync ps{p.pipe_counters, p.pipe_counters + a.rf, p.pipe_counters + 2 * a.rf};
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.nsm);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = smem_pipe();
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_pipe, a, ps);
-    if (e != cudaSuccess) return e;
-    if (mark) mark(mk, K_ROW, s);
-    k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, smem_rowinvw(), s>>>(a);
-    if (mark) mark(mk, K_ROW, s);
-    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw<8>(), s>>>(a);
-    if (mark) mark(mk, K_COL_INV, s);
-    return cudaGetLastError();
-  }
-  const bool eoi = v == 8;
-  const bool rn = v == 7 || eoi;
-  const bool col8 = v != 1, rowstage = v == 0 || v == 5;
-  const int cw = col8 ? 8 : 4;
-  a.nblk_colfwd = kW_N2 / cw;
+  if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);  // experiment switches (tools/ab.sh)
+  const int nsm = p.nsm > 0 ? p.nsm : 148;
+  a.nblk_colfwd = kW_N2 / 8;
   k_transpose_n<<<(kW_H / 32) * (kW_N2 / 32), 256, 0, s>>>(a);
   if (mark) mark(mk, K_TRANSPOSE, s);
+  const int rows = kW_N1 / 2 + 1;
+  // 2 row pairs per half; the SMs left over run D
+  const int per = (rows + 2 * nsm - 1) / (2 * nsm);
+  const int rgrid = (rows + 2 * per - 1) / (2 * per);
   for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
-    const int items = (kW_N2 / cw) * gc;
-    if (eoi) {
-      k_colw<8, true, true><<<items < nsm ? items : nsm, 256, smem_colw<8, true>(), s>>>(a, g0, gc);
-    } else if (col8) {
-      k_colw<8, true><<<items < nsm ? items : nsm, 256, smem_colw<8, true>(), s>>>(a, g0, gc);
-    } else {
-      k_colw<4, false><<<items < 2 * nsm ? items : 2 * nsm, 128, smem_colw<4, false>(), s>>>(a, g0, gc);
-    }
+    const bool last = g0 + gc >= a.rf;
+    const int items = (kW_N2 / 8) * gc;
+    k_colt<<<items < nsm ? items : nsm, 256, smem_colt(), s>>>(a, g0, gc);
     if (mark) mark(mk, K_COL_FWD, s);
-    if (rn && g0 + gc >= a.rf) {
-      k_scalars_w<<<1, 256, 0, s>>>(a);  // D then runs beside the last row launch
-    } else if (g0 + gc >= a.rf) {
-      // fork: all column partials exist -> scalars and the non-birth part on the side stream
-      cudaEventRecord(p.ev_fork, s);
-      cudaStreamWaitEvent(p.side, p.ev_fork, 0);
-      k_scalars_w<<<1, 256, 0, p.side>>>(a);
-      k_dvec<<<4 * nsm, 256, 0, p.side>>>(a);
-      cudaEventRecord(p.ev_join, p.side);
-    }
-    const int rows = kW_N1 / 2 + 1;
-    if (rn) {
-      // 2 row pairs per half; the SMs left over run D (programmatic dependent launch: k_dvec
-      // starts once every row CTA is resident and waits for the row grid before it exits)
-      const int per = (rows + 2 * nsm - 1) / (2 * nsm);
-      const int grid = (rows + 2 * per - 1) / (2 * per);
-      if (eoi) {
-        k_rown<true><<<grid, 256, smem_rown(), s>>>(a, g0, gc, g0 == 0);
-      } else {
-        k_rown<false><<<grid, 256, smem_rown(), s>>>(a, g0, gc, g0 == 0);
-      }
-      if (g0 + gc >= a.rf) {
-        if (mark) mark(mk, K_ROW, s);
-        const int free = nsm - grid;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
-        cfg.blockDim = dim3(256);
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[0].val.programmaticStreamSerializationAllowed = mark ? 0 : 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_dvec, a);
-        if (e != cudaSuccess) return e;
-      }
-    } else if (rowstage) {
-      k_roww<true><<<rows < nsm ? rows : nsm, 128, smem_roww<true>(), s>>>(a, g0, gc, g0 == 0);
+    if (last) k_scalars_w<<<1, 256, 0, s>>>(a);  // every column partial exists
+    static const int rowv = getenv("AGK_ROWV") ? atoi(getenv("AGK_ROWV")) : 1;
+    if (rowv == 2) {
+      k_rowd2<<<2 * rgrid < nsm ? 2 * rgrid : rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
+    } else if (rowv == 3) {
+      k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
     } else {
-      k_roww<false><<<rows < 2 * nsm ? rows : 2 * nsm, 128, smem_roww<false>(), s>>>(a, g0, gc, g0 == 0);
+      k_rowd<false><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
     }
     if (mark) mark(mk, K_ROW, s);
+    if (last) {
+      // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
+      // every row CTA is resident and waits for the row grid before it exits)
+      const int free = nsm - rgrid;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
+      cfg.blockDim = dim3(256);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = mark ? 0 : 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k_dvec, a);
+      if (e != cudaSuccess) return e;
+      if (mark) mark(mk, K_DVEC, s);
+    }
   }
   k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, smem_rowinvw(), s>>>(a);
-  if (mark) mark(mk, K_ROW, s);
-  // join the side stream (scalars + D) before the inverse column pass
-  if (!rn) cudaStreamWaitEvent(s, p.ev_join, 0);
-  static const bool civ4 = getenv("AGK_CIV") && atoi(getenv("AGK_CIV")) == 4;
-  if (col8 && !civ4) {
-    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw<8>(), s>>>(a);
-  } else {
-    k_colinvw<4><<<kW_N2 / 8, 128, smem_colinvw<4>(), s>>>(a);
-  }
+  if (mark) mark(mk, K_ROW_INV, s);
+  k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw(), s>>>(a);
   if (mark) mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }
