@@ -336,8 +336,9 @@ __device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, cons
 // exchange patterns (i = 32k + lane and i = 32 lane + l) conflict-free, and since each warp owns
 // one chunk per row, eight warps can share one tile without synchronising.
 __device__ __forceinline__ int tile_idx(int i, int w) { return i * 8 + (w ^ ((i ^ (i >> 5)) & 7)); }
+// step A alone (registers + twiddle table): the caller may interleave other work before step B
 template <int SIGN, bool HALFZERO>
-__device__ __forceinline__ void warp_fft1024_t(double2 (&v)[32], double2* T, int w, const double2* tw, int lane) {
+__device__ __forceinline__ void warp_fft1024_a(double2 (&v)[32], const double2* tw, int lane) {
   if constexpr (HALFZERO) {
     dft_halfzero<32, SIGN>(v);
   } else {
@@ -348,6 +349,21 @@ __device__ __forceinline__ void warp_fft1024_t(double2 (&v)[32], double2* T, int
     const double2 t = tw[k * 32 + lane];
     v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
   }
+}
+// exchange through the tile + step B
+template <int SIGN>
+__device__ __forceinline__ void warp_fft1024_tb(double2 (&v)[32], double2* T, int w, int lane) {
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[tile_idx(32 * k + lane, w)] = v[k];
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; ++l) v[l] = T[tile_idx(32 * lane + l, w)];
+  Dft<32, SIGN>::run(v);
+}
+template <int SIGN, bool HALFZERO>
+__device__ __forceinline__ void warp_fft1024_t(double2 (&v)[32], double2* T, int w, const double2* tw, int lane) {
+  warp_fft1024_a<SIGN, HALFZERO>(v, tw, lane);
   __syncwarp();
 #pragma unroll
   for (int k = 0; k < 32; ++k) T[tile_idx(32 * k + lane, w)] = v[k];

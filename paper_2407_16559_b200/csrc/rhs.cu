@@ -435,7 +435,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   const int ngroups = (rf + g - 1) / g;
   const char* fe = getenv("AGK_FAST");
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
-  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 4 : 0);
+  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 3 : 0);
   p->nsm = 148;
 }
 

@@ -13,7 +13,8 @@
 //   k_rowd        : per row pair (k1, N1-k1) x rank: 1024-pt FFTs of the even and odd samples,
 //                   the decimation-in-time radix-2 stage fused into the conjugate-pair split,
 //                   w*A*B summed over ranks in registers. Two independent 4-warp halves per CTA.
-//   k_rowinvw     : inverse row transform of the Hermitian half-rows, inverse twiddle -> G.
+//                   The last launch also runs the inverse row transform of the Hermitian rows and
+//                   the inverse four-step twiddle -> G.
 //   k_colinvw     : per column pair, 1024-pt inverse FFT of G_a + i G_b (two real outputs),
 //                   epilogue birth + D, where D (death/sources/shattering) came from k_dvec.
 #include "rhs_common.cuh"
@@ -34,7 +35,6 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 32x32 tiles.
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 32x32 tiles.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   if (a.skip && *a.skip) return;
@@ -87,6 +87,16 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
     cp_async_commit();
   };
+  // the tile as full 128-byte row lines: slots (o & 1) * 1024 + 8 (o >> 1) + c of rank g's rows
+  auto store_tile = [&](int item) {
+    const int o = item / gcount, g = item % gcount;
+    double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+#pragma unroll 8
+    for (int it = 0; it < kW_N1 / 32; ++it) {
+      const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
+      yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
+    }
+  };
   if (it0 < it1) prefetch(it0);
   __syncthreads();
   double nl[16];
@@ -125,7 +135,15 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
-    if (!(a.dbg & 1)) warp_fft1024_t<-1, true>(v, T, w, tw, lane);
+    {
+      warp_fft1024_a<-1, true>(v, tw, lane);
+      // the previous item's tile goes out while step A runs (one instruction stream, so the
+      // stores interleave with the transform); the first item stores its own (not yet written)
+      // tile to its own destination, which its real store overwrites later in program order
+      if (!(a.dbg & 2)) store_tile(item == it0 ? item : item - 1);
+      __syncthreads();  // every warp has read the tile: it is free for the exchanges
+      warp_fft1024_tb<-1>(v, T, w, lane);
+    }
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
 #pragma unroll
@@ -141,22 +159,14 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       red[w][3] = s3;
     }
     __syncthreads();
-    if (!(a.dbg & 2)) {
-      double2* __restrict__ yg = a.y + (int64_t)g * P + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
-#pragma unroll 8
-      for (int it = 0; it < kW_N1 / 32; ++it) {
-        const int idx = tid + 256 * it, row = idx >> 3, c = idx & 7;
-        yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
-      }
-    }
     if (tid < 4) {
       double t = 0.0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) t += red[q][tid];
       a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
     }
-    __syncthreads();
   }
+  if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
 }
 
 // Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
@@ -164,14 +174,18 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
 // loads its 1024 samples (contiguous: the permuted Y layout) and transforms them to E (h = 0) or
 // O (h = 1); the half then forms X[q'] = E + W_2048^q' O, X[q' + 1024] = E - W_2048^q' O of both
 // rows, the conjugate-pair split and w*A*B, accumulated over ranks in registers.
+// LAST (the launch of the last rank group): the half then runs the inverse row transform of its
+// accumulated Hermitian row k1 (2 warps, radix-2 DIF + 1024-point inverse FFTs) and the inverse
+// four-step twiddle, writing G in place of the accumulator row.
 // Launched with 2 row pairs per half (grid = ceil(513 / 4) = 129 CTAs at N1 = 1024) so the SMs
 // left over run the non-birth part D concurrently (k_dvec, programmatic dependent launch).
-template <bool PREF>
+template <bool LAST>
 __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, int first) {
   extern __shared__ double2 smem[];
   double2* X = smem;               // 8 regions: per half E1, O1 (row k1), E2, O2 (row N1-k1)
   double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
   double2* twh = tw + 1024;        // W_2048^j, j < 1024
+  __shared__ double2 tkk[8][32];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
@@ -184,24 +198,19 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     twh[i] = __ldg(a.tw2048h + i);
   }
   __syncthreads();
-  const double2* Xh = X + hf * 4 * kXR;
+  double2* Xh = X + hf * 4 * kXR;
   double2* Xw = X + w * kXR;
-  double2 v[32];
   for (int k1 = 2 * blockIdx.x + hf; k1 < nrows; k1 += 2 * gridDim.x) {
     const int row = rho == 0 ? k1 : (n1 - k1) & (n1 - 1);
     const double2* __restrict__ rsrc = a.y + (int64_t)row * kW_N2 + h * (kW_N2 / 2);
     double2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j];
-    if (PREF && k1 == 2 * (int)blockIdx.x + hf) {
-#pragma unroll
-      for (int r = 0; r < 32; ++r) v[r] = rsrc[lane + 32 * r];
-    }
     for (int g = 0; g < gcount; ++g) {
       const double wt = a.uniq_weight[g0 + g];
       const double2* __restrict__ src = rsrc + (int64_t)g * P;
-      if (PREF) {
-      } else if (!(a.dbg & 64)) {
+      double2 v[32];
+      if (!(a.dbg & 64)) {
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       } else {
@@ -212,17 +221,6 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
-      if (PREF) {
-        // next item's samples into the idle transform registers (in flight during the split)
-        const int nk = g + 1 < gcount ? k1 : k1 + 2 * (int)gridDim.x;
-        const int ng = g + 1 < gcount ? g + 1 : 0;
-        if (nk < nrows) {
-          const int nrow = rho == 0 ? nk : (n1 - nk) & (n1 - 1);
-          const double2* __restrict__ ns = a.y + (int64_t)ng * P + (int64_t)nrow * kW_N2 + h * (kW_N2 / 2);
-#pragma unroll
-          for (int r = 0; r < 32; ++r) v[r] = ns[lane + 32 * r];
-        }
-      }
       bar_sync(bar, 128);
       if (!(a.dbg & 32))
 #pragma unroll
@@ -245,143 +243,33 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       }
       bar_sync(bar, 128);
     }
+    if constexpr (!LAST) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j] = acc[j];
-  }
-}
-
-// Row pass, variant 2: one row pair (k1, N1-k1) per CTA at a time, TWO ranks per step (warps
-// 0-3 rank g, warps 4-7 rank g+1; warp (rho, h) = (row, even/odd samples)). Each of the 256
-// threads then owns 4 bins q' (8 accumulators: q' and q' + 1024), which keeps the register
-// accumulators beside the transform without spilling; the next step's samples are loaded into
-// the (idle) transform registers before the split, so the loads overlap the split.
-__global__ void __launch_bounds__(256, 1) k_rowd2(RhsArgs a, int g0, int gcount, int first) {
-  extern __shared__ double2 smem[];
-  double2* X = smem;               // 8 regions: [rank slot][E1, O1, E2, O2]
-  double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
-  double2* twh = tw + 1024;        // W_2048^j, j < 1024
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (a.skip && *a.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, gi = w >> 2, hw = w & 3, rho = hw >> 1, h = hw & 1;
-  const int n1 = a.n1;
-  const int64_t P = (int64_t)kW_N1 * kW_N2;
-  const int nrows = n1 / 2 + 1;
-  for (int i = tid; i < 1024; i += blockDim.x) {
-    tw[i] = __ldg(a.tw32 + i);
-    twh[i] = __ldg(a.tw2048h + i);
-  }
-  __syncthreads();
-  double2* Xw = X + w * kXR;
-  const bool pref = !(a.dbg & 128);
-  auto load = [&](double2 (&v)[32], int kk, int g) {
-    const int row = rho == 0 ? kk : (n1 - kk) & (n1 - 1);
-    const double2* __restrict__ src = a.y + (int64_t)g * P + (int64_t)row * kW_N2 + h * (kW_N2 / 2);
+      for (int j = 0; j < 16; ++j) a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j] = acc[j];
+    } else {
+      // inverse row transform of the accumulated row k1 (rho = 0 warps; regions 2, 3 hold the row)
+      double2* Ar = Xh + 2 * kXR;  // 2120 >= 2048 contiguous entries
 #pragma unroll
-    for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
-  };
-  int k1 = blockIdx.x;
-  if (k1 >= nrows) return;
-  double2 v[32];
-  if (gi < gcount) load(v, k1, gi);
-  for (; k1 < nrows; k1 += gridDim.x) {
-    double2 acc[8];
+      for (int j = 0; j < 16; ++j) Ar[ht + 128 * j] = acc[j];
+      bar_sync(bar, 128);
+      if (rho == 0) {
+        double2 v[32];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int q = tid + 256 * (j & 3) + 1024 * (j >> 2);
-      acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + q];
-    }
-    for (int g = 0; g < gcount; g += 2) {
-      const bool act = g + gi < gcount;
-      if (!pref && act) load(v, k1, g + gi);
-      if (act) {
-        warp_fft1024<-1, false>(v, Xw, tw, lane);
+        for (int r = 0; r < 32; ++r) {
+          const double2 lo = Ar[lane + 32 * r], hi = Ar[1024 + lane + 32 * r];
+          v[r] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), cconj(twh[lane + 32 * r]));
+        }
+        warp_fft1024<+1, false>(v, Xw, tw, lane);
+        // T[c2], c2 = 2(lane + 32k) + h; G = T W_P^{-c2 k1} = T W_P^{-(2 lane + h) k1} W_P^{-64 k1 k}
+        const double2 base = tw_p<+1>(a.twp, (uint32_t)((2 * lane + h) * k1));
+        tkk[w][lane] = tw_p<+1>(a.twp, (uint32_t)((64 * k1 * lane) & (P - 1)));
         __syncwarp();
+        double2* __restrict__ gr = a.acc + (int64_t)k1 * kW_N2;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
+        for (int k = 0; k < 32; ++k) gr[2 * (lane + 32 * k) + h] = cmul(v[k], cmul(base, tkk[w][k]));
       }
-      if (pref) {
-        if (g + 2 + gi < gcount) {
-          load(v, k1, g + 2 + gi);
-        } else if (k1 + (int)gridDim.x < nrows && gi < gcount) {
-          load(v, k1 + gridDim.x, gi);
-        }
-      }
-      __syncthreads();
-      const int nr = gcount - g < 2 ? gcount - g : 2;
-      for (int s = 0; s < nr; ++s) {
-        const double wt = a.uniq_weight[g0 + g + s];
-        const double2* Xs = X + 4 * s * kXR;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int qp = tid + 256 * j;
-          // partner bins of q' and q' + 1024 in row N1-k1 (row 0 pairs with itself at N2 - q)
-          const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
-          const double sa = (k1 == 0 && qp == 0) ? 1.0 : -1.0;
-          const double2 e1 = Xs[qp], o1 = Xs[kXR + qp];
-          const double2 e2 = Xs[2 * kXR + m], o2 = Xs[3 * kXR + m];
-          const double2 t1 = cmul(o1, twh[qp]), t2 = cmul(o2, twh[m]);
-          const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
-          const double2 pa = make_double2(e2.x + sa * t2.x, e2.y + sa * t2.y);
-          const double2 pb = make_double2(e2.x - sa * t2.x, e2.y - sa * t2.y);
-          const double2 ra = split_product(xa, pa), rb = split_product(xb, pb);
-          acc[j].x += wt * ra.x;
-          acc[j].y += wt * ra.y;
-          acc[j + 4].x += wt * rb.x;
-          acc[j + 4].y += wt * rb.y;
-        }
-      }
-      __syncthreads();
+      bar_sync(bar, 128);  // the regions are reused by the next row pair
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int q = tid + 256 * (j & 3) + 1024 * (j >> 2);
-      a.acc[(int64_t)k1 * kW_N2 + q] = acc[j];
-    }
-  }
-}
-
-// inverse row transform of the Hermitian half-rows k1 = 0..N1/2 (2 warps per row, radix-2 DIF),
-// inverse four-step twiddle -> G rows; block 0 also reduces the moment partials into the scalars
-__global__ void __launch_bounds__(128) k_rowinvw(RhsArgs a) {
-  extern __shared__ double2 smem[];
-  double2* X = smem;               // 4 regions: two rows' halves
-  double2* tw = X + 4 * kXR;
-  double2* twh = tw + 1024;
-  __shared__ double2 tkk[4][32];
-  if (a.skip && *a.skip) return;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, sub = w >> 1, h = w & 1;
-  const int P = kW_N1 * kW_N2;
-  for (int i = tid; i < 1024; i += blockDim.x) {
-    tw[i] = __ldg(a.tw32 + i);
-    twh[i] = __ldg(a.tw2048h + i);
-  }
-  __syncthreads();
-  const int nrows = kW_N1 / 2 + 1;
-  for (int k1b = 2 * blockIdx.x; k1b < nrows; k1b += 2 * gridDim.x) {
-    const int k1 = k1b + sub;
-    double2 v[32];
-    if (k1 < nrows) {
-      const double2* __restrict__ ar = a.acc + (int64_t)k1 * kW_N2;
-#pragma unroll
-      for (int r = 0; r < 32; ++r) v[r] = ar[lane + 32 * r];
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const double2 hi = ar[1024 + lane + 32 * r];
-        v[r] = h == 0 ? cadd(v[r], hi) : cmul(csub(v[r], hi), cconj(twh[r * 32 + lane]));
-      }
-      warp_fft1024<+1, false>(v, X + w * kXR, tw, lane);
-    }
-    __syncthreads();  // all rows of this pass loaded before G overwrites acc rows
-    if (k1 < nrows) {
-      // T[c2], c2 = 2(lane + 32k) + h; G = T W_P^{-c2 k1} = T W_P^{-(2 lane + h) k1} W_P^{-64 k1 k}
-      const double2 base = tw_p<+1>(a.twp, (uint32_t)((2 * lane + h) * k1));
-      tkk[w][lane] = tw_p<+1>(a.twp, (uint32_t)((64 * k1 * lane) & (P - 1)));
-      __syncwarp();
-      double2* __restrict__ gr = a.acc + (int64_t)k1 * kW_N2;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) gr[2 * (lane + 32 * k) + h] = cmul(v[k], cmul(base, tkk[w][k]));
-    }
-    __syncthreads();
   }
 }
 
@@ -516,7 +404,6 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
 
 static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
-static size_t smem_rowinvw() { return (size_t)(4 * kXR + 2048) * sizeof(double2); }
 static size_t smem_colinvw() {
   constexpr int CW = 8;
   const size_t tile = (size_t)(kW_N1 / 2 + 1) * (2 * CW + 1);
@@ -530,16 +417,14 @@ cudaError_t rhs_w_set_smem_limits() {
   SET(k_colt, smem_colt());
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
-  SET(k_rowd2, smem_rowd());
-  SET(k_rowinvw, smem_rowinvw());
   SET(k_colinvw<8>, smem_colinvw());
 #undef SET
   return cudaSuccess;
 }
 
-// One RHS: transpose | per rank group: column pass, row pass | scalars before the last row pass,
-// D beside it | inverse row pass | inverse column pass with the epilogue. 7 launches for <= 16
-// unique ranks (the plan's `launches`).
+// One RHS: transpose of n | per rank group, column pass | row pass (the last one also runs the inverse row
+// transform; the scalars go just before it and D beside it) | inverse column pass with the
+// epilogue. 6 launches for <= 16 unique ranks (the plan's `launches`).
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
   RhsArgs a = a0;
@@ -558,36 +443,30 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const int items = (kW_N2 / 8) * gc;
     k_colt<<<items < nsm ? items : nsm, 256, smem_colt(), s>>>(a, g0, gc);
     if (mark) mark(mk, K_COL_FWD, s);
-    if (last) k_scalars_w<<<1, 256, 0, s>>>(a);  // every column partial exists
-    static const int rowv = getenv("AGK_ROWV") ? atoi(getenv("AGK_ROWV")) : 1;
-    if (rowv == 2) {
-      k_rowd2<<<2 * rgrid < nsm ? 2 * rgrid : rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
-    } else if (rowv == 3) {
-      k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
-    } else {
+    if (!last) {
       k_rowd<false><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
+      if (mark) mark(mk, K_ROW, s);
+      continue;
     }
+    k_scalars_w<<<1, 256, 0, s>>>(a);  // every column partial exists
+    k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
     if (mark) mark(mk, K_ROW, s);
-    if (last) {
-      // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
-      // every row CTA is resident and waits for the row grid before it exits)
-      const int free = nsm - rgrid;
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
-      cfg.blockDim = dim3(256);
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = mark ? 0 : 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      cudaError_t e = cudaLaunchKernelEx(&cfg, k_dvec, a);
-      if (e != cudaSuccess) return e;
-      if (mark) mark(mk, K_DVEC, s);
-    }
+    // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
+    // every row CTA is resident and waits for the row grid before it exits)
+    const int free = nsm - rgrid;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = mark ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_dvec, a);
+    if (e != cudaSuccess) return e;
+    if (mark) mark(mk, K_DVEC, s);
   }
-  k_rowinvw<<<(kW_N1 / 2 + 2) / 2 < 2 * nsm ? (kW_N1 / 2 + 2) / 2 : 2 * nsm, 128, smem_rowinvw(), s>>>(a);
-  if (mark) mark(mk, K_ROW_INV, s);
   k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw(), s>>>(a);
   if (mark) mark(mk, K_COL_INV, s);
   return cudaGetLastError();
