@@ -31,6 +31,43 @@ __device__ __forceinline__ void block_sum(double (&x)[NV], double* red) {
   __syncthreads();
 }
 
+// Reduce the per-CTA moment partials [ub][blk][4] into tot[ub*4+q] (global or shared scratch)
+// in a fixed order, by all warps of the calling CTA (blockDim a multiple of 32): a warp sums 8
+// outputs at once, lane l taking blocks l, l+32, ... with all 64 loads of a 256-block chunk in
+// flight, then a shuffle tree. Bitwise reproducible; ~one memory round trip per chunk.
+__device__ __forceinline__ void reduce_partials_wide(const RhsArgs& a, int nblk, double* tot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nout = a.rf * 4;
+  for (int p0 = warp; p0 < nout; p0 += 8 * nw) {
+    double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int b0 = 0; b0 < nblk; b0 += 256) {
+      double x[8][8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int p = p0 + j * nw;
+        const double* __restrict__ src = a.partials + (int64_t)(p >> 2) * nblk * 4 + (p & 3);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int b = b0 + lane + 32 * u;
+          x[j][u] = (p < nout && b < nblk) ? src[(int64_t)b * 4] : 0.0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[j] += x[j][u];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], off);
+      const int p = p0 + j * nw;
+      if (lane == 0 && p < nout) tot[p] = s[j];
+    }
+  }
+}
+
+// Register-light variant for kernels that carry transforms (one warp per output, fixed order).
 // Reduce the per-CTA moment partials [ub][blk][4] into tot[ub*4+q] (global scratch), fixed
 // order, by all warps of the calling CTA (blockDim a multiple of 32).
 __device__ __forceinline__ void reduce_partials(const RhsArgs& a, int nblk, double* tot) {

@@ -35,25 +35,25 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 32x32 tiles.
+// n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 64 x 64 tiles, 16 elements
+// per thread in flight, 256-byte coalesced rows both ways.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   if (a.skip && *a.skip) return;
-  __shared__ double t[32][33];
+  __shared__ double t[64][65];
   const double* __restrict__ n = a.n.get();
-  const int bx = blockIdx.x % (kW_N2 / 32), by = blockIdx.x / (kW_N2 / 32);  // n2 tile, n1 tile
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int bx = blockIdx.x % (kW_N2 / 64), by = blockIdx.x / (kW_N2 / 64);  // n2 tile, n1 tile
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  double v[16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int n1 = by * 32 + ty + 8 * q, n2 = bx * 32 + tx;
-    const int64_t i = (int64_t)n1 * kW_N2 + n2;
-    t[ty + 8 * q][tx] = i < a.m ? n[i] : 0.0;
+  for (int q = 0; q < 16; ++q) {
+    const int64_t i = (int64_t)(by * 64 + ty + 4 * q) * kW_N2 + bx * 64 + tx;
+    v[q] = i < a.m ? n[i] : 0.0;
   }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) t[ty + 4 * q][tx] = v[q];
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int n2 = bx * 32 + ty + 8 * q, n1 = by * 32 + tx;
-    a.ng[(int64_t)n2 * kW_H + n1] = t[tx][ty + 8 * q];
-  }
+  for (int q = 0; q < 16; ++q) a.ng[(int64_t)(bx * 64 + ty + 4 * q) * kW_H + by * 64 + tx] = t[tx][ty + 4 * q];
 }
 
 // Y layout (per rank, [k1][slot], 2048 slots per row): the row transform's first radix-2 stage
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 __global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
   if (a.skip && *a.skip) return;
   double* tot = a.scalars + a.r + 2;
-  reduce_partials(a, a.nblk_colfwd, tot);
+  reduce_partials_wide(a, a.nblk_colfwd, tot);
   __syncthreads();
   if (threadIdx.x == 0) finalize_scalars(a, tot, a.n.get()[0]);
 }
@@ -404,6 +404,12 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
 
 static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
+template <int CW>
+static size_t smem_colinvw_t() {
+  const size_t tile = (size_t)(kW_N1 / 2 + 1) * (2 * CW + 1);
+  return ((tile > (size_t)CW * kXR ? tile : (size_t)CW * kXR) + 1024 + (size_t)kW_H * CW) * sizeof(double2);
+}
+static size_t smem_colinvw4() { return smem_colinvw_t<4>(); }
 static size_t smem_colinvw() {
   constexpr int CW = 8;
   const size_t tile = (size_t)(kW_N1 / 2 + 1) * (2 * CW + 1);
@@ -418,6 +424,7 @@ cudaError_t rhs_w_set_smem_limits() {
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
   SET(k_colinvw<8>, smem_colinvw());
+  SET(k_colinvw<4>, smem_colinvw4());
 #undef SET
   return cudaSuccess;
 }
@@ -431,7 +438,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
   if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);  // experiment switches (tools/ab.sh)
   const int nsm = p.nsm > 0 ? p.nsm : 148;
   a.nblk_colfwd = kW_N2 / 8;
-  k_transpose_n<<<(kW_H / 32) * (kW_N2 / 32), 256, 0, s>>>(a);
+  k_transpose_n<<<(kW_H / 64) * (kW_N2 / 64), 256, 0, s>>>(a);
   if (mark) mark(mk, K_TRANSPOSE, s);
   const int rows = kW_N1 / 2 + 1;
   // 2 row pairs per half; the SMs left over run D
@@ -467,7 +474,12 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     if (e != cudaSuccess) return e;
     if (mark) mark(mk, K_DVEC, s);
   }
-  k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw(), s>>>(a);
+  static const bool civ4 = getenv("AGK_CIV") && atoi(getenv("AGK_CIV")) == 4;
+  if (civ4) {
+    k_colinvw<4><<<kW_N2 / 8, 128, smem_colinvw4(), s>>>(a);
+  } else {
+    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw(), s>>>(a);
+  }
   if (mark) mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }
