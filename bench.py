@@ -142,16 +142,23 @@ def survey_flops(m, rf):
 
 
 def kernel_counts(cls, m, r, rf, plan, first, g):
-    """Algorithmic HBM bytes and fp64 flops of ONE launch of a four-step kernel."""
+    """Algorithmic HBM bytes and fp64 flops of ONE launch of a fast-path kernel class at P = 2^21
+    (DESIGN.md §3): the bytes each kernel must move at minimum, the flops of 5 N log2 N per
+    transform plus the pointwise work."""
     log2p, n1, n2, gs = plan
     p = 1 << log2p
     l1, l2 = n1.bit_length() - 1, n2.bit_length() - 1
-    if cls == "col_fwd":
-        return 8 * m + 16 * m * g + 16 * p * g, g * (5 * p * l1 + 6 * p)
-    if cls == "row":
-        return 16 * p * g + 8 * p * (0 if first else 1) + 8 * p, g * (5 * p * l2 + 9 * p) + 5 * (p // 2) * l2
-    if cls == "col_inv":
-        return 8 * p + 8 * m + 8 * m * r + 8 * m, 5 * (p // 2) * l1 + 4 * m * r
+    if cls == "transpose":
+        return 8 * m + 8 * (p // 2), 0
+    if cls == "col_fwd":  # n grid + (U, V) columns + Y write, per rank in the group
+        return 8 * (p // 2) + 16 * (p // 2) * g + 16 * p * g, g * (5 * p * l1 + 6 * p)
+    if cls == "row":  # Y read + accumulator rows (+ read when not the first group); last: inverse rows
+        acc = 16 * (n1 // 2 + 1) * n2
+        return 16 * p * g + acc * (1 if first else 2), g * (5 * p * l2 + 9 * p) + 5 * (p // 2) * l2
+    if cls == "dvec":  # U^T rows, n, D
+        return 8 * m * r + 16 * m, 2 * m * r
+    if cls == "col_inv":  # G half rows, D, S
+        return 16 * (n1 // 2 + 1) * n2 + 16 * m, 5 * (p // 2) * l1
     return 8 * m * (2 * r + 2), survey_flops(m, rf)
 
 

@@ -1,5 +1,6 @@
 // internal.h — device-side parameter blocks shared by the RHS, stepper and API translation units.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -80,6 +81,10 @@ struct RhsPlan {
   int launches;  // kernels per RHS
   // SM count (grid sizing of the fast path)
   int nsm;
+  // fast path: TMA descriptor of Y viewed as [gsize * N1 rows][2 * N2 doubles], 128-byte
+  // swizzle, box 16 doubles x 256 rows (column-tile stores); valid when ytmap_ok
+  CUtensorMap ytmap;
+  int ytmap_ok;
 };
 
 // kernel classes for per-launch timing

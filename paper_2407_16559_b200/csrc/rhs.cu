@@ -437,6 +437,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
   p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 3 : 0);
   p->nsm = 148;
+  p->ytmap_ok = 0;
 }
 
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }

@@ -102,6 +102,33 @@ __device__ __forceinline__ void finalize_scalars(const RhsArgs& a, const double*
   a.scalars[a.r + 1] = mono;
 }
 
+// The same, by a whole CTA: each thread finishes its ranks' w_a and gain terms (the loads of
+// all ranks in flight together), then thread 0 sums the gains in rank order. sh: 2 r doubles.
+__device__ __forceinline__ void finalize_scalars_cta(const RhsArgs& a, const double* tot, double n0, double* sh) {
+  for (int ra = threadIdx.x; ra < a.r; ra += blockDim.x) {
+    const int code = a.rank_map[ra];
+    const bool sw = code >= kSwap;
+    const int ub = sw ? code - kSwap : code;
+    const double A0 = tot[ub * 4 + 0], A1 = tot[ub * 4 + 1];
+    const double B0 = tot[ub * 4 + 2], B1 = tot[ub * 4 + 3];
+    const double su0 = sw ? B0 : A0, su1 = sw ? B1 : A1;
+    const double sv0 = sw ? A0 : B0, sv1 = sw ? A1 : B1;
+    a.scalars[ra] = sv0 + a.v0[ra] * n0;  // w_a = sum_j V_aj n_j
+    sh[2 * ra] = su1 * sv0 + su0 * sv1;
+    sh[2 * ra + 1] = a.u0[ra] * sv1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pair = 0.0, mono = 0.0;
+    for (int ra = 0; ra < a.r; ++ra) {
+      pair += sh[2 * ra];
+      mono += sh[2 * ra + 1];
+    }
+    a.scalars[a.r] = pair;
+    a.scalars[a.r + 1] = mono;
+  }
+}
+
 // Epilogue for output index jo >= 1: S = birth - death [+ shattering loss] [+ sources], with the
 // death row sum sum_a U_sa w_a given (ascending a, as rhs.cpp:24-46 accumulates it)
 __device__ __forceinline__ double epilogue_rs(const RhsArgs& a, const double* __restrict__ n, int64_t jo,

@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   double nl[16];
   double2 base = czero();
   int cur_o = -1;
-  const int64_t P = (int64_t)kW_N1 * kW_N2;
   for (int item = it0; item < it1; ++item) {
     const int o = item / gcount, g = item % gcount, ub = g0 + g;
     const int n2 = col_of(o);
@@ -167,6 +166,113 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     }
   }
   if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
+}
+
+// Column pass with TMA tile stores: as k_colt, but the finished tile is laid out in TMA's 128-byte
+// swizzle (chunk c of row i at c ^ (i & 7)) and written back by four asynchronous bulk tensor
+// stores issued by one thread, which drain while the next item's operands arrive and its step A
+// runs. The exchange keeps its own swizzle (tile_idx), so a barrier separates the last exchange
+// read from the first output write; the tile is reused only after the bulk stores have read it.
+__device__ __forceinline__ int tma_idx(int i, int c) { return i * 8 + (c ^ (i & 7)); }
+__global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, const __grid_constant__ CUtensorMap ytm) {
+  extern __shared__ double2 smem_raw[];
+  double2* T = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
+  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
+  __shared__ double red[8][4];
+  __shared__ double2 tk[8][32];
+  if (a.skip && *a.skip) return;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int items = (kW_N2 / 8) * gcount;
+  const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
+  const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
+  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
+  double2* Sw = S + w * kW_H;
+  auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * w + (o & 1); };
+  auto prefetch = [&](int item) {
+    const int o = item / gcount, ub = g0 + item % gcount;
+    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
+    cp_async_commit();
+  };
+  const uint32_t tsm = (uint32_t)__cvta_generic_to_shared(T);
+  const uint64_t tmp = reinterpret_cast<uint64_t>(&ytm);
+  if (it0 < it1) prefetch(it0);
+  __syncthreads();
+  double nl[16];
+  double2 base = czero();
+  int cur_o = -1;
+  for (int item = it0; item < it1; ++item) {
+    const int o = item / gcount, g = item % gcount, ub = g0 + g;
+    const int n2 = col_of(o);
+    if (o != cur_o) {
+      cur_o = o;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
+      base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
+      tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    double2 v[32];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const double2 uv = Sw[lane + 32 * r];
+      const double x = uv.x * nl[r], y = uv.y * nl[r];
+      v[r] = make_double2(x, y);
+      const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
+      if (i >= 1) {
+        const double sz = (double)(i + 1);
+        s0 += x;
+        s1 += sz * x;
+        s2 += y;
+        s3 += sz * y;
+      }
+    }
+#pragma unroll
+    for (int r = 16; r < 32; ++r) v[r] = czero();
+    __syncwarp();
+    if (item + 1 < it1) prefetch(item + 1);
+    warp_fft1024_a<-1, true>(v, tw, lane);
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    __syncthreads();  // the previous tile has been read by its bulk stores
+    warp_fft1024_tb<-1>(v, T, w, lane);
+    __syncthreads();  // every exchange read is done before the output writes (other swizzle)
+#pragma unroll
+    for (int k = 0; k < 32; ++k) T[tma_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    if (lane == 0) {
+      red[w][0] = s0;
+      red[w][1] = s1;
+      red[w][2] = s2;
+      red[w][3] = s3;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && !(a.dbg & 2)) {
+      // rows g * 1024 + 256 b .. +255, doubles 2 * slot0 .. +15 of Y viewed as [rows][4096]
+      const int x = 2 * ((o & 1) * (kW_N2 / 2) + 8 * (o >> 1));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int yrow = g * kW_N1 + 256 * b;
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                     ::"l"(tmp), "r"(x), "r"(yrow), "r"(tsm + b * 256 * 128) : "memory");
+      }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    if (tid < 4) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += red[q][tid];
+      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
@@ -275,11 +381,13 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 
 // w_a, pair and monomer gains from the column pass' partials (one CTA, fixed order)
 __global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
+  extern __shared__ double sh[];  // 2 r
   if (a.skip && *a.skip) return;
+  const double n0 = a.n.get()[0];
   double* tot = a.scalars + a.r + 2;
   reduce_partials_wide(a, a.nblk_colfwd, tot);
   __syncthreads();
-  if (threadIdx.x == 0) finalize_scalars(a, tot, a.n.get()[0]);
+  finalize_scalars_cta(a, tot, n0, sh);
 }
 
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
@@ -402,6 +510,7 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   }
 }
 
+static size_t smem_colm() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2) + 1024; }
 static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
 template <int CW>
@@ -421,6 +530,7 @@ cudaError_t rhs_w_set_smem_limits() {
 #define SET(fn, bytes) \
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
   SET(k_colt, smem_colt());
+  SET(k_colm, smem_colm());
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
   SET(k_colinvw<8>, smem_colinvw());
@@ -448,14 +558,19 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
-    k_colt<<<items < nsm ? items : nsm, 256, smem_colt(), s>>>(a, g0, gc);
+    static const bool tma = !(getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 0);
+    if (tma && p.ytmap_ok) {
+      k_colm<<<items < nsm ? items : nsm, 256, smem_colm(), s>>>(a, g0, gc, p.ytmap);
+    } else {
+      k_colt<<<items < nsm ? items : nsm, 256, smem_colt(), s>>>(a, g0, gc);
+    }
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
       k_rowd<false><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
       if (mark) mark(mk, K_ROW, s);
       continue;
     }
-    k_scalars_w<<<1, 256, 0, s>>>(a);  // every column partial exists
+    k_scalars_w<<<1, 256, 2 * a.r * sizeof(double), s>>>(a);  // every column partial exists
     k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
     if (mark) mark(mk, K_ROW, s);
     // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
