@@ -64,7 +64,7 @@ class GpuWorkspace {
   explicit GpuWorkspace(const ModelSpec& model, int device = -1) : m_(model.m) {
     model.validate();
     const auto* lr = std::get_if<LowRankFactors>(&model.kernel);
-    if (!lr) throw std::invalid_argument("the B200 path serves low-rank kernels (dense kernels are out of scope)");
+    const auto* dk = std::get_if<DenseKernel>(&model.kernel);  // dense path: rhs_dense.cu
     std::vector<uint64_t> k;
     std::vector<double> rate;
     for (const auto& [kk, rr] : model.sources.rates) {
@@ -73,9 +73,13 @@ class GpuWorkspace {
     }
     agk_model_desc d{};
     d.m = model.m;
-    d.r = lr->r;
-    d.u = lr->u.data();
-    d.v = lr->v.data();
+    if (lr) {
+      d.r = lr->r;
+      d.u = lr->u.data();
+      d.v = lr->v.data();
+    } else {
+      d.k = dk->k.data();
+    }
     d.variant = static_cast<int>(model.variant);
     d.source_k = k.data();
     d.source_rate = rate.data();

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define AGK_ABI_VERSION 1
+#define AGK_ABI_VERSION 2
 
 typedef enum {
   AGK_OK = 0,
@@ -53,6 +53,10 @@ typedef struct {
   size_t num_sources;
   double shatter_rate;      /* aggregation_shattering: lambda >= 0 */
   int device;               /* CUDA device ordinal; -1 = current device */
+  const double* k;          /* DenseKernel (kernels.hpp:38-43): m x m row-major, K(i,j) =
+                               k[(i-1)*m + j-1]. Non-NULL selects the dense path (rhs.cpp
+                               dense branches 37-45, 153-159, 197-205) and r/u/v are ignored;
+                               m <= 2^17. NULL: the low-rank factors u/v. (ABI version 2) */
 } agk_model_desc;
 
 /* Injected right-hand sides: the reference's stepper tests bind these to RhsFn

@@ -99,12 +99,24 @@ static void plan_transform(const fft_plan* p, double* a, int invert) {
 /* ---------------------------------------------------------------- RHS (rhs.cpp) */
 
 static int model_ok(const ora_model* md) {
-  return md && md->m >= 2 && md->r >= 1 && md->u && md->v;
+  return md && md->m >= 2 && (md->k || (md->r >= 1 && md->u && md->v));
 }
 
-/* kernel_row_sums, low-rank branch (rhs.cpp:24-36) */
+/* K(i,j) of a DenseKernel (kernels.hpp:42), 1-based */
+static double dense_at(const ora_model* md, size_t i, size_t j) { return md->k[(i - 1) * md->m + (j - 1)]; }
+
+/* kernel_row_sums (rhs.cpp:24-46): low-rank branch 27-36, dense branch 37-45 */
 static void row_sums(const ora_model* md, const double* n, double* rowsum) {
   const size_t m = md->m, r = md->r;
+  if (md->k) {
+    for (size_t s = 0; s < m; ++s) {
+      const double* row = md->k + s * m;
+      double acc = 0.0;
+      for (size_t j = 0; j < m; ++j) acc += row[j] * n[j];
+      rowsum[s] = acc;
+    }
+    return;
+  }
   for (size_t s = 0; s < m; ++s) rowsum[s] = 0.0;
   for (size_t a = 0; a < r; ++a) {
     double w = 0.0;
@@ -152,6 +164,15 @@ static void dedupe(const ora_model* md, double* weight, unsigned char* skip) {
 int ora_birth_term(const ora_model* md, const double* n, double* out) {
   if (!model_ok(md)) return -1;
   const size_t m = md->m, r = md->r;
+  if (md->k) { /* dense branch (rhs.cpp:153-159) */
+    out[0] = 0.0;
+    for (size_t s = 2; s <= m; ++s) {
+      double acc = 0.0;
+      for (size_t i = 1; i < s; ++i) acc += dense_at(md, i, s - i) * n[i - 1] * n[s - i - 1];
+      out[s - 1] = 0.5 * acc;
+    }
+    return 0;
+  }
   const size_t padded = next_pow2(2 * m) * ORA_PAD_FACTOR;
   fft_plan plan;
   if (plan_init(&plan, padded)) return -1;
@@ -205,7 +226,12 @@ int ora_shattering_terms(const ora_model* md, const double* n, double lambda, do
   double* rowsum = (double*)malloc(m * sizeof(double));
   row_sums(md, n, rowsum);
   double pair_gain = 0.0, mono_gain = 0.0;
-  for (size_t a = 0; a < r; ++a) { /* rhs.cpp:185-196 */
+  if (md->k) { /* dense branch (rhs.cpp:197-205) */
+    for (size_t i = 2; i <= m; ++i)
+      for (size_t j = 2; j <= m; ++j) pair_gain += (double)(i + j) * dense_at(md, i, j) * n[i - 1] * n[j - 1];
+    for (size_t j = 2; j <= m; ++j) mono_gain += (double)j * dense_at(md, 1, j) * n[j - 1];
+  }
+  for (size_t a = 0; a < (md->k ? 0 : r); ++a) { /* rhs.cpp:185-196 */
     double su0 = 0.0, su1 = 0.0, sv0 = 0.0, sv1 = 0.0;
     for (size_t i = 2; i <= m; ++i) {
       const double size = (double)i;
@@ -254,6 +280,7 @@ int ora_eval_rhs(const ora_model* md, const double* n, double* out) {
 }
 
 static double entry(const ora_model* md, size_t i, size_t j) {
+  if (md->k) return dense_at(md, i, j);
   double acc = 0.0;
   for (size_t a = 0; a < md->r; ++a) acc += md->u[(i - 1) * md->r + a] * md->v[a * md->m + (j - 1)];
   return acc;

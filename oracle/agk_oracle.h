@@ -7,6 +7,8 @@
  * (/root/reference/proj, C++20):
  *   - low-rank RHS   : src/rhs.cpp:24-46 (row sums), 87-151 (birth), 162-168 (death),
  *                      170-210 (shattering), 212-235 (eval_rhs), 284-294 (Euler bound)
+ *   - dense RHS      : the DenseKernel branches of the same functions, rhs.cpp:37-45 (row sums),
+ *                      153-159 (birth), 197-205 (shattering gains)
  *   - FFT            : src/fft.cpp:64-137 (built-in radix-2; the reference build here has no FFTW)
  *   - steppers       : src/steppers.cpp:11-50 (helpers), 94-159 (steps), 161-300 (controllers)
  *   - run loop       : src/simulator.cpp:112-229
@@ -51,6 +53,8 @@ typedef struct {
   const double* source_rate;
   size_t num_sources;
   double shatter_rate;
+  const double* k; /* DenseKernel (kernels.hpp:38-43): m x m row-major, K(i,j) = k[(i-1)*m + j-1];
+                      when non-NULL the kernel is dense and r/u/v are ignored */
 } ora_model;
 
 /* Returns 0 on success, -1 on invalid argument (the reference throws std::invalid_argument). */

@@ -49,7 +49,7 @@ static void fft_ld(ld* a, size_t n, int inv) {
 
 /* eval_rhs with every intermediate in long double; rounding to double only at the end */
 int ora_eval_rhs_truth(const ora_model* md, const double* n, double* out) {
-  if (!md || md->m < 2 || md->r < 1) return -1;
+  if (!md || md->m < 2 || md->r < 1 || md->k) return -1; /* low-rank kernels only */
   const size_t m = md->m, r = md->r, P = np2(2 * m);
   ld* z = (ld*)malloc(2 * P * sizeof(ld));
   ld* acc = (ld*)calloc(2 * P, sizeof(ld));

@@ -38,7 +38,7 @@ _dp = C.POINTER(C.c_double)
 class _Model(C.Structure):
     _fields_ = [("m", C.c_size_t), ("r", C.c_size_t), ("u", _dp), ("v", _dp), ("variant", C.c_int),
                 ("source_k", C.POINTER(C.c_uint64)), ("source_rate", _dp),
-                ("num_sources", C.c_size_t), ("shatter_rate", C.c_double)]
+                ("num_sources", C.c_size_t), ("shatter_rate", C.c_double), ("k", _dp)]
 
 
 class _Control(C.Structure):
@@ -84,14 +84,23 @@ def _p(a):
 
 @dataclass
 class Model:
-    """Low-rank model in the reference's layouts (kernels.hpp:26-35, rhs.hpp:32-40)."""
+    """Model in the reference's layouts (kernels.hpp:26-43, rhs.hpp:32-40): low-rank factors
+    u (m, r) and v (r, m), or a DenseKernel `k` (m, m) — then u and v may be None."""
     u: np.ndarray           # (m, r) row-major
     v: np.ndarray           # (r, m) row-major
     variant: int = AGGREGATION
     sources: list = field(default_factory=list)   # [(k, rate)], 1-based k
     shatter_rate: float = 0.0
+    k: np.ndarray = None    # dense kernel (m, m) row-major, K(i,j) = k[i-1, j-1]
 
     def __post_init__(self):
+        if self.k is not None:
+            self.k = np.ascontiguousarray(self.k, dtype=np.float64)
+            m = self.k.shape[0]
+            if self.u is None:
+                self.u = np.zeros((m, 1))
+            if self.v is None:
+                self.v = np.zeros((1, m))
         self.u = np.ascontiguousarray(self.u, dtype=np.float64)
         self.v = np.ascontiguousarray(self.v, dtype=np.float64)
         if self.u.ndim == 1:
@@ -112,7 +121,8 @@ class Model:
     def c(self):
         return _Model(self.m, self.r, _p(self.u), _p(self.v), self.variant,
                       self._sk.ctypes.data_as(C.POINTER(C.c_uint64)), _p(self._sr),
-                      len(self.sources), float(self.shatter_rate))
+                      len(self.sources), float(self.shatter_rate),
+                      _p(self.k) if self.k is not None else None)
 
 
 class OracleError(ValueError):
@@ -265,6 +275,15 @@ def brownian_factors(m, alpha):
     u = np.stack([p, 1.0 / p], axis=1)
     v = np.stack([1.0 / p, p], axis=0)
     return u, v
+
+
+def free_molecular_dense(m):
+    """DenseKernel of the free-molecular kernel (kernels.cpp:49-51, build_dense 103-): K(x,y) =
+    (cbrt x + cbrt y)^2 sqrt(1/x + 1/y), x, y = 1..m."""
+    x = np.arange(1, m + 1, dtype=np.float64)
+    c = np.cbrt(x)
+    s = c[:, None] + c[None, :]
+    return s * s * np.sqrt(1.0 / x[:, None] + 1.0 / x[None, :])
 
 
 def brownian_plus2_factors(m):

@@ -23,12 +23,19 @@ ModelSpec to_spec(const ora_model* md) {
   ModelSpec spec;
   spec.variant = static_cast<ModelVariant>(md->variant);
   spec.m = md->m;
-  LowRankFactors f;
-  f.m = md->m;
-  f.r = md->r;
-  f.u.assign(md->u, md->u + md->m * md->r);
-  f.v.assign(md->v, md->v + md->m * md->r);
-  spec.kernel = std::move(f);
+  if (md->k) {
+    DenseKernel d;
+    d.m = md->m;
+    d.k.assign(md->k, md->k + md->m * md->m);
+    spec.kernel = std::move(d);
+  } else {
+    LowRankFactors f;
+    f.m = md->m;
+    f.r = md->r;
+    f.u.assign(md->u, md->u + md->m * md->r);
+    f.v.assign(md->v, md->v + md->m * md->r);
+    spec.kernel = std::move(f);
+  }
   for (size_t q = 0; q < md->num_sources; ++q)
     spec.sources.rates.emplace_back(static_cast<std::size_t>(md->source_k[q]), md->source_rate[q]);
   spec.shatter_rate = md->shatter_rate;

@@ -48,7 +48,7 @@ _dp = C.POINTER(C.c_double)
 class _ModelDesc(C.Structure):
     _fields_ = [("m", C.c_size_t), ("r", C.c_size_t), ("u", _dp), ("v", _dp), ("variant", C.c_int),
                 ("source_k", C.POINTER(C.c_uint64)), ("source_rate", _dp), ("num_sources", C.c_size_t),
-                ("shatter_rate", C.c_double), ("device", C.c_int)]
+                ("shatter_rate", C.c_double), ("device", C.c_int), ("k", _dp)]
 
 
 class _Control(C.Structure):
@@ -178,14 +178,25 @@ def _out_like(x, m):
 
 @dataclass
 class Model:
-    """ModelSpec with LowRankFactors, reference layouts: u (m, r), v (r, m) (kernels.hpp:26-35)."""
-    u: np.ndarray
-    v: np.ndarray
+    """ModelSpec, reference layouts: LowRankFactors u (m, r), v (r, m) (kernels.hpp:26-35), or a
+    DenseKernel k (m, m) (kernels.hpp:38-43; then u and v may be None)."""
+    u: Optional[np.ndarray]
+    v: Optional[np.ndarray]
     variant: int = AGGREGATION
     sources: Sequence = field(default_factory=list)  # [(k, rate)], 1-based k (SourceTerm)
     shatter_rate: float = 0.0
+    k: Optional[np.ndarray] = None  # dense K(i,j) = k[i-1, j-1]
 
     def __post_init__(self):
+        if self.k is not None:
+            self.k = np.ascontiguousarray(self.k, dtype=np.float64)
+            mk = self.k.shape[0]
+            if self.k.shape != (mk, mk):
+                raise ValueError("dense kernel must be m x m")
+            if self.u is None:
+                self.u = np.zeros((mk, 1))
+            if self.v is None:
+                self.v = np.zeros((1, mk))
         self.u = np.ascontiguousarray(self.u, dtype=np.float64)
         self.v = np.ascontiguousarray(self.v, dtype=np.float64)
         if self.u.ndim == 1:
@@ -220,7 +231,8 @@ class RhsWorkspace:
         sr = np.array([rt for _, rt in model.sources] or [0.0], dtype=np.float64)
         d = _ModelDesc(model.m, model.r, model.u.ctypes.data_as(_dp), model.v.ctypes.data_as(_dp), model.variant,
                        sk.ctypes.data_as(C.POINTER(C.c_uint64)), sr.ctypes.data_as(_dp), len(model.sources),
-                       float(model.shatter_rate), device)
+                       float(model.shatter_rate), device,
+                       model.k.ctypes.data_as(_dp) if model.k is not None else None)
         _check(lib.agk_rhs_create(C.byref(d), C.byref(self._h)))
         self.m = model.m
         self.model = model
@@ -465,7 +477,7 @@ def run(ws: RhsWorkspace, cfg: SimulationConfig) -> RunReport:
                      rep.total_accepted, rep.total_rejects, rep.wall_seconds)
 
 
-KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv", "transpose", "dvec", "row_inv")
+KERNEL_CLASSES = ("small", "col_fwd", "row", "col_inv", "transpose", "dvec", "row_inv", "dense_rows", "dense_birth")
 
 
 def eval_rhs_timed(ws: RhsWorkspace, n_dev, out_dev, count: int) -> float:

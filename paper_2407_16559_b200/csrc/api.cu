@@ -257,6 +257,72 @@ int model_flags(const agk_rhs* h) {
 
 }  // namespace
 
+// DenseKernel model (rhs.cpp dense branches; rhs_dense.cu): K is copied to the device once.
+static agk_status create_dense(const agk_model_desc* d, std::unique_ptr<agk_rhs> h, agk_rhs** out) {
+  const int64_t m = (int64_t)d->m;
+  if (d->m > ((size_t)1 << 17)) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "dense kernel m > 2^17 is not supported");
+  h->kind = AGK_RHS_MODEL;
+  h->m = m;
+  h->r = 0;
+  h->rf = 0;
+  h->variant = d->variant;
+  h->lambda = d->shatter_rate;
+  RhsPlan& p = h->plan;
+  p = RhsPlan{};
+  p.dense = 1;
+  p.launches = 3 + (d->variant == AGK_AGGREGATION_SHATTERING ? 1 : 0);
+  agk_status st = alloc_common(h.get());
+  agk_rhs* hp = h.get();
+  auto cleanup_fail = [&](agk_status s2) {
+    g_create_error = hp->err;
+    for (void* q : hp->allocs) cudaFree(q);
+    hp->allocs.clear();
+    return s2;
+  };
+  if (st) return cleanup_fail(st);
+#define CK_D(x, what)                                                        \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess) return cleanup_fail(cuda_fail(hp, e_, what));     \
+  } while (0)
+  RhsArgs& a = h->base;
+  double *kd, *drow, *dpair, *dpart, *scalars;
+  CK_D(dalloc(hp, &kd, (size_t)m * m), "alloc dense kernel");
+  CK_D(cudaMemcpy(kd, d->k, (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice), "upload dense kernel");
+  CK_D(dalloc(hp, &drow, (size_t)m), "alloc row sums");
+  CK_D(dalloc(hp, &dpair, (size_t)m), "alloc gain terms");
+  CK_D(dalloc(hp, &dpart, (size_t)dense_chunks(m) * m), "alloc birth partials");
+  CK_D(dalloc(hp, &scalars, 8), "alloc scalars");
+  int64_t* sk = nullptr;
+  double* sr = nullptr;
+  if (d->variant == AGK_AGGREGATION_SOURCES && d->num_sources > 0) {
+    std::vector<int64_t> hk(d->num_sources);
+    for (size_t q = 0; q < d->num_sources; ++q) hk[q] = (int64_t)d->source_k[q];
+    CK_D(dalloc(hp, &sk, d->num_sources), "alloc sources");
+    CK_D(dalloc(hp, &sr, d->num_sources), "alloc sources");
+    CK_D(cudaMemcpy(sk, hk.data(), hk.size() * sizeof(int64_t), cudaMemcpyHostToDevice), "upload sources");
+    CK_D(cudaMemcpy(sr, d->source_rate, d->num_sources * sizeof(double), cudaMemcpyHostToDevice), "upload sources");
+    h->nsrc = (int)d->num_sources;
+  }
+  a.m = m;
+  a.r = 0;
+  a.rf = 0;
+  a.kd = kd;
+  a.drow = drow;
+  a.dpair = dpair;
+  a.dpart = dpart;
+  a.scalars = scalars;
+  a.flags = model_flags(hp);
+  a.lambda = d->shatter_rate;
+  a.src_k = sk;
+  a.src_rate = sr;
+  a.nsrc = h->nsrc;
+  CK_D(cudaStreamSynchronize(hp->stream), "create sync");
+#undef CK_D
+  *out = h.release();
+  return AGK_OK;
+}
+
 extern "C" {
 
 void agk_control_defaults(agk_control* c) {
@@ -301,7 +367,7 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
   *out = nullptr;
   // ModelSpec::validate (rhs.cpp:63-72) and SourceTerm::validate (rhs.cpp:48-61)
   if (d->m < 2) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "truncation size m must be >= 2");
-  if (d->r < 1 || !d->u || !d->v) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "kernel factors missing");
+  if (!d->k && (d->r < 1 || !d->u || !d->v)) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "kernel factors missing");
   if (d->m > ((size_t)1 << 22)) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "m > 2^22 is not supported");
   if (d->variant < 0 || d->variant > 2) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "unknown model variant");
   if (d->variant == AGK_AGGREGATION_SOURCES) {
@@ -322,6 +388,7 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
     g_create_error = h->err;
     return st;
   }
+  if (d->k) return create_dense(d, std::move(h), out);
   const int64_t m = (int64_t)d->m;
   const int r = (int)d->r;
   h->kind = AGK_RHS_MODEL;

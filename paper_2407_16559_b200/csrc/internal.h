@@ -68,6 +68,12 @@ struct RhsArgs {
   const double2* tw32;     // [k1*32 + l] = W_1024^{l k1}
   const double2* tw2048h;  // [r*32 + l] = W_2048^{l + 32 r}
   double* dvec;            // m: the non-birth part of S (death, sources, shattering)
+  // dense kernel (rhs_dense.cu): K m x m row-major, row sums, shattering-gain terms per row,
+  // per-chunk birth partials (dense_chunks(m) x m)
+  const double* kd;
+  double* drow;
+  double* dpair;
+  double* dpart;
   int dbg;                 // experiment switches (AGK_DBG), 0 in production
 };
 
@@ -75,6 +81,7 @@ struct RhsArgs {
 struct RhsPlan {
   int small;     // 1: single-CTA path (P <= 4096)
   int fast;      // 1: warp-synchronous path (P = 2^21)
+  int dense;     // 1: DenseKernel path (rhs_dense.cu); no FFT
   int log2p;
   int n1, n2, c, cp;
   int gsize;     // ranks per group in the four-step path
@@ -88,7 +95,7 @@ struct RhsPlan {
 };
 
 // kernel classes for per-launch timing
-enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4, K_DVEC = 5, K_ROW_INV = 6 };
+enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4, K_DVEC = 5, K_ROW_INV = 6, K_DENSE_ROWS = 7, K_DENSE_BIRTH = 8 };
 
 // host-side launchers (rhs.cu)
 void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);
@@ -104,6 +111,13 @@ cudaError_t rhs_set_smem_limits();
 cudaError_t rhs_w_set_smem_limits();
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk);
+
+// dense-kernel path (rhs_dense.cu)
+int dense_chunks(int64_t m);
+cudaError_t rhs_dense_launch(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
+                             void* mk);
+// per-CTA maxima of the dense row sums of n into rmax[nblk] (Euler bound)
+cudaError_t launch_dense_rowmax(const RhsArgs& md, VecRef n, double* rmax, int nblk, cudaStream_t s);
 
 // Injected fakes (AGK_RHS_DECAY, ...) as one elementwise kernel.
 cudaError_t fake_rhs_launch(int kind, double param, VecRef n, double* out, int64_t m,

@@ -437,6 +437,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
   p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 3 : 0);
   p->nsm = 148;
+  p->dense = 0;
   p->ytmap_ok = 0;
 }
 
@@ -536,6 +537,7 @@ static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStre
 }
 
 static cudaError_t rhs_launch_impl(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
+  if (p.dense) return rhs_dense_launch(p, a, s, mk ? mark_cb : nullptr, mk);
   if (p.fast) return rhs_w_launch(p, a, s, mk ? mark_cb : nullptr, mk);
   switch (p.log2p) {
     case 2: return launch_small<4>(a, s, mk);

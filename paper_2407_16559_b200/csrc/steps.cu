@@ -496,8 +496,12 @@ cudaError_t launch_euler_bound(const RhsArgs& md, VecRef n, double a, double* au
                                cudaStream_t s) {
   double* dots = aux + naux * 4;
   double* rmax = aux + naux * 3;
-  k_rank_dots<<<dim3(naux, md.r), kRedThreads, 0, s>>>(md.v, n, md.m, dots);
-  k_rowsum_max<<<naux, kRedThreads, md.r * sizeof(double), s>>>(md.ut, md.r, md.m, dots, naux, rmax);
+  if (md.kd) {
+    AGK_CK(launch_dense_rowmax(md, n, rmax, naux, s));
+  } else {
+    k_rank_dots<<<dim3(naux, md.r), kRedThreads, 0, s>>>(md.v, n, md.m, dots);
+    k_rowsum_max<<<naux, kRedThreads, md.r * sizeof(double), s>>>(md.ut, md.r, md.m, dots, naux, rmax);
+  }
   k_euler_final<<<1, 1, 0, s>>>(rmax, naux, a, out_dev);
   return cudaGetLastError();
 }
@@ -520,7 +524,9 @@ cudaError_t build_step_graph(int body, int stepper, const RhsEnqueue& rhs, const
   double* rmax = b.aux + b.naux * 3;
   double* dots = b.aux + b.naux * 4;
   k_state_moments<<<b.naux, kRedThreads, 0, s>>>(state, m, mom);
-  if (model) {
+  if (model && model->kd) {
+    AGK_CK(launch_dense_rowmax(*model, state, rmax, b.naux, s));
+  } else if (model) {
     k_rank_dots<<<dim3(b.naux, model->r), kRedThreads, 0, s>>>(model->v, state, m, dots);
     k_rowsum_max<<<b.naux, kRedThreads, model->r * sizeof(double), s>>>(model->ut, model->r, m, dots, b.naux, rmax);
   }

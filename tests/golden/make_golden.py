@@ -51,6 +51,29 @@ def rhs_cases():
     return idx
 
 
+def dense_cases():
+    """DenseKernel (free-molecular, kernels.cpp:49-51) RHS goldens: the reference's dense branches
+    (rhs.cpp:37-45, 153-159, 197-205) on seeded states."""
+    ref = O.Oracle("reference")
+    rng = np.random.Generator(np.random.MT19937(0x5EED5EED + 1))
+    out = {}
+    idx = 0
+    for m in (2, 3, 17, 64, 257, 1000):
+        k = O.free_molecular_dense(m)
+        for var in VARIANTS:
+            srcs = [(1, 1.0), (min(m, 10), 0.1)] if var == O.SOURCES else []
+            md = O.Model(None, None, var, srcs, 0.01 if var == O.SHATTERING else 0.0, k=k)
+            n = rng.random(m)
+            out[f"c{idx}_meta"] = np.array([m, var], dtype=np.float64)
+            out[f"c{idx}_n"] = n
+            out[f"c{idx}_S"] = ref.eval_rhs(md, n)
+            out[f"c{idx}_bound"] = np.array([ref.euler_stability_bound(md, n, 0.25)])
+            idx += 1
+    out["count"] = np.array([idx])
+    np.savez_compressed(os.path.join(HERE, "golden_dense.npz"), **out)
+    return idx
+
+
 RUNS = [
     # (name, kernel, alpha, m, variant, sources, lambda, stepper, mode, tol/tau, t_end, snapshots)
     ("agg_const_rk4_m256", "constant", 0.0, 256, O.AGGREGATION, [], 0.0, O.RK4, O.ADAPTIVE, 1e-8, 10.0, [1.0, 10.0]),
@@ -88,6 +111,11 @@ def run_cases():
     return len(res)
 
 
+if __name__ == "__main__" and "--dense-only" in sys.argv:
+    print("dense cases:", dense_cases())
+    sys.exit(0)
+
 if __name__ == "__main__":
     print("rhs cases", rhs_cases())
+    print("dense cases", dense_cases())
     print("run cases", run_cases())

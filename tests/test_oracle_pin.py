@@ -256,3 +256,42 @@ def test_port_matches_golden_run_fixtures(oracle_port):
         assert (r["total_rhs_evals"], r["total_accepted"], r["total_rejects"]) == \
                (c["total_rhs_evals"], c["total_accepted"], c["total_rejects"]), name
         assert np.array_equal(r["final_state"], np.array(c["final_state"])), name
+
+
+# ---------------------------------------------------------------- DenseKernel branches (§8f item 3)
+
+@pytest.mark.parametrize("m", [2, 3, 17, 64, 300])
+@pytest.mark.parametrize("variant", [O.AGGREGATION, O.SOURCES, O.SHATTERING])
+def test_port_dense_bitwise_equals_reference(oracle_port, oracle_ref, m, variant):
+    """The C restatement of the dense branches (rhs.cpp:37-45, 153-159, 197-205) is bitwise the
+    reference's eval_rhs / terms / Euler bound on a DenseKernel (free-molecular, kernels.cpp:49-51)."""
+    k = O.free_molecular_dense(m)
+    src = [(1, 1.0), (min(m, 5), 0.1)] if variant == O.SOURCES else []
+    md = O.Model(None, None, variant, src, 0.02, k=k)
+    n = np.random.default_rng(m).random(m)
+    for fn in ("eval_rhs", "birth_term", "death_term"):
+        assert np.array_equal(getattr(oracle_port, fn)(md, n), getattr(oracle_ref, fn)(md, n)), fn
+    assert np.array_equal(oracle_port.shattering_terms(md, n, 0.02), oracle_ref.shattering_terms(md, n, 0.02))
+    assert oracle_port.euler_stability_bound(md, n, 0.25) == oracle_ref.euler_stability_bound(md, n, 0.25)
+
+
+def test_port_dense_advance_bitwise(oracle_port, oracle_ref):
+    m = 128
+    md = O.Model(None, None, O.SOURCES, [(1, 1.0)], 0.0, k=O.free_molecular_dense(m))
+    n = np.random.default_rng(3).random(m) * 0.1
+    for stepper in (O.RK2, O.RK4, O.RKF45):
+        a = oracle_port.advance(n, 0.01, O.Control(stepper=stepper, tol=1e-9), model=md)
+        b = oracle_ref.advance(n, 0.01, O.Control(stepper=stepper, tol=1e-9), model=md)
+        assert np.array_equal(a["state"], b["state"]) and a["rhs_evals"] == b["rhs_evals"]
+
+
+def test_port_matches_golden_dense_fixtures(oracle_port):
+    """tests/golden/golden_dense.npz: generated from the reference itself (make_golden.py)."""
+    g = np.load(os.path.join(GOLDEN, "golden_dense.npz"))
+    for c in range(int(g["count"][0])):
+        m, var = (int(x) for x in g[f"c{c}_meta"])
+        src = [(1, 1.0), (min(m, 10), 0.1)] if var == O.SOURCES else []
+        md = O.Model(None, None, var, src, 0.01 if var == O.SHATTERING else 0.0, k=O.free_molecular_dense(m))
+        n = g[f"c{c}_n"]
+        assert np.array_equal(oracle_port.eval_rhs(md, n), g[f"c{c}_S"]), c
+        assert oracle_port.euler_stability_bound(md, n, 0.25) == g[f"c{c}_bound"][0], c
