@@ -133,6 +133,16 @@ typedef struct {
 
 int ora_run(ora_rhs* rhs, size_t m, const ora_run_desc* d, ora_run_report* rep);
 
+/* Reference writers (report_io.cpp:32-98, bench.cpp:126-171), exported by oracle/_ref only: the
+ * byte-compatibility checkers of paper_2407_16559_b200/report_io.py. abort_reason: "" when the
+ * run completed. Bench: schemes[ns] (ORA_RK*), cells (mode[nc], value[nc]); results row-major
+ * [scheme][cell] with status 1 = completed; notes[ns*nc] (NULL entries = ""). */
+int ref_write_run_outputs(const ora_run_report* rep, size_t m, const double* snapshot_times,
+                          const char* abort_reason, double wall_seconds, const char* dir);
+int ref_write_bench_outputs(const int* schemes, size_t ns, const int* cell_mode, const double* cell_value,
+                            size_t nc, const uint64_t* evals, const uint64_t* accepted, const uint64_t* rejected,
+                            const double* wall, const int* completed, const char* const* notes, const char* dir);
+
 #ifdef __cplusplus
 }
 #endif

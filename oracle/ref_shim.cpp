@@ -11,6 +11,9 @@
 #include <vector>
 
 #include "agk_oracle.h"
+#include "aggkin/bench.hpp"
+#include "aggkin/config.hpp"
+#include "aggkin/report_io.hpp"
 #include "aggkin/rhs.hpp"
 #include "aggkin/simulator.hpp"
 #include "aggkin/steppers.hpp"
@@ -228,3 +231,66 @@ int ref_run(ora_rhs* f, size_t m, const ora_run_desc* d, ora_run_report* rep) tr
 }
 
 }  // extern "C"
+
+extern "C" int ref_write_run_outputs(const ora_run_report* r, size_t m, const double* snapshot_times,
+                                     const char* abort_reason, double wall_seconds, const char* dir) {
+  try {
+    RunReport rep;
+    for (size_t q = 0; q < r->num_records && q < r->records_capacity; ++q) {
+      const ora_record& x = r->records[q];
+      ObservableRecord o;
+      o.t = x.t;
+      o.tau = x.tau;
+      o.density = x.density;
+      o.mass = x.mass;
+      o.m2 = x.m2;
+      o.error_estimate = x.error_estimate;
+      o.rhs_evals = x.rhs_evals;
+      o.rejects = x.rejects;
+      rep.records.push_back(o);
+    }
+    for (size_t q = 0; q < r->num_snapshots_taken; ++q)
+      rep.snapshots.emplace_back(snapshot_times[q], std::vector<double>(r->snapshots + q * m, r->snapshots + (q + 1) * m));
+    rep.final_state.t = r->final_t;
+    if (r->final_state) rep.final_state.n.assign(r->final_state, r->final_state + m);
+    rep.termination = r->termination ? Termination::aborted : Termination::completed;
+    rep.abort_reason = abort_reason ? abort_reason : "";
+    rep.abort_t = r->abort_t;
+    rep.abort_tau = r->abort_tau;
+    rep.total_rhs_evals = r->total_rhs_evals;
+    rep.total_accepted = r->total_accepted;
+    rep.total_rejects = r->total_rejects;
+    rep.wall_seconds = wall_seconds;
+    write_run_outputs(rep, dir);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+extern "C" int ref_write_bench_outputs(const int* schemes, size_t ns, const int* cell_mode, const double* cell_value,
+                                       size_t nc, const uint64_t* evals, const uint64_t* accepted,
+                                       const uint64_t* rejected, const double* wall, const int* completed,
+                                       const char* const* notes, const char* dir) {
+  try {
+    ExperimentConfig cfg;
+    for (size_t i = 0; i < ns; ++i) cfg.bench_schemes.push_back(static_cast<StepperKind>(schemes[i]));
+    for (size_t c = 0; c < nc; ++c) cfg.bench_cells.push_back(BenchCell{static_cast<StepMode>(cell_mode[c]), cell_value[c]});
+    std::vector<BenchResult> res(ns * nc);
+    for (size_t i = 0; i < ns * nc; ++i) {
+      res[i].scheme = cfg.bench_schemes[i / nc];
+      res[i].cell = cfg.bench_cells[i % nc];
+      res[i].rhs_evals = evals[i];
+      res[i].accepted = accepted[i];
+      res[i].rejected = rejected[i];
+      res[i].wall_seconds = wall[i];
+      res[i].completed = completed[i] != 0;
+      res[i].note = (notes && notes[i]) ? notes[i] : "";
+    }
+    write_bench_outputs(cfg, res, dir);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
