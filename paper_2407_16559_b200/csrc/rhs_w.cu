@@ -558,7 +558,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
-    static const bool tma = !(getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 0);
+    static const bool tma = getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 1;  // measured slower
     if (tma && p.ytmap_ok) {
       k_colm<<<items < nsm ? items : nsm, 256, smem_colm(), s>>>(a, g0, gc, p.ytmap);
     } else {

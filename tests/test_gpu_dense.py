@@ -21,7 +21,7 @@ SRC = [(1, 1.0), (5, 0.1), (1, 0.5)]
 
 def make(agk, m, variant=O.AGGREGATION, lam=0.01):
     K = O.free_molecular_dense(m)
-    src = SRC if variant == O.SOURCES else []
+    src = [(k, r) for k, r in SRC if k <= m] if variant == O.SOURCES else []  # k in 1..m (rhs.cpp:50-60)
     om = O.Model(None, None, variant, src, lam, k=K)
     return om, agk.RhsWorkspace(agk.Model(None, None, variant, src, lam, k=K))
 
@@ -41,6 +41,13 @@ def test_dense_eval_rhs(agk, oracle_port, m, variant):
         got = agk.eval_rhs(ws, n)
         assert rel_max_diff(got, want) <= TOL
     assert ws.evals() == 2
+
+
+def test_dense_source_outside_range_rejected(agk):
+    # ModelSpec::validate -> SourceTerm::validate throws invalid_argument (rhs.cpp:50-60, 63-66)
+    K = O.free_molecular_dense(4)
+    with pytest.raises(ValueError):
+        agk.RhsWorkspace(agk.Model(None, None, O.SOURCES, [(5, 0.1)], 0.0, k=K))
 
 
 @pytest.mark.parametrize("m", [64, 1000, 4097])
