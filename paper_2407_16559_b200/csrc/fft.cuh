@@ -159,6 +159,12 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
 }
+// Bulk L2 prefetch of a contiguous range (one instruction, no registers, no completion to wait
+// on): pulls the next work item's operands from HBM into L2 a whole transform ahead, so the
+// later register/shared loads of them hit L2.
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -347,6 +353,32 @@ __device__ __forceinline__ void warp_fft1024_a(double2 (&v)[32], const double2* 
 #pragma unroll
   for (int k = 1; k < 32; ++k) {
     const double2 t = tw[k * 32 + lane];
+    v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
+  }
+}
+// L1-resident read-only loads (twiddle tables read from global memory) and L1-bypassing
+// streaming loads, so a small L1 (most of the SRAM given to shared memory) keeps the tables.
+__device__ __forceinline__ double2 ldg_keep(const double2* p) {
+  double2 r;
+  asm("ld.global.nc.L1::evict_last.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+// step A with the W_1024 table in global memory (L1)
+template <int SIGN, bool HALFZERO>
+__device__ __forceinline__ void warp_fft1024_ag(double2 (&v)[32], const double2* tw, int lane) {
+  if constexpr (HALFZERO) {
+    dft_halfzero<32, SIGN>(v);
+  } else {
+    Dft<32, SIGN>::run(v);
+  }
+#pragma unroll
+  for (int k = 1; k < 32; ++k) {
+    const double2 t = ldg_keep(tw + k * 32 + lane);
     v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
   }
 }

@@ -59,6 +59,7 @@ struct RhsArgs {
   double2* acc;         // (n1/2 + 1) * n2 accumulator, then G rows
   double* partials;     // rf * nblk_colfwd * 4
   double* scalars;      // r (w_a) + 2 (pair_gain, mono_gain)
+  int pfd;           // fast path: L2 prefetch distance of the column/row passes (items)
   int nblk_colfwd;
   TwTable tw_n1, tw_n2, tw_small;
   TwoLevel twp;

@@ -435,7 +435,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   const int ngroups = (rf + g - 1) / g;
   const char* fe = getenv("AGK_FAST");
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
-  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 3 : 0);
+  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);
   p->nsm = 148;
   p->dense = 0;
   p->ytmap_ok = 0;
@@ -444,7 +444,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
 size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
 size_t rhs_acc_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)(p.n1 / 2 + 1) * p.n2; }
 size_t rhs_partial_elems(const RhsPlan& p, int rf) {
-  const size_t nblk = p.small ? 1 : (size_t)(p.n2 / 2);  // enough for any column-block width >= 2
+  const size_t nblk = p.small ? 1 : (size_t)p.n2;  // any column-block width >= 2, or one block per column
   return (size_t)rf * nblk * 4;
 }
 

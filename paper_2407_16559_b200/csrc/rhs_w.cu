@@ -38,6 +38,7 @@ __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 64 x 64 tiles, 16 elements
 // per thread in flight, 256-byte coalesced rows both ways.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the column pass' prologue may start
   if (a.skip && *a.skip) return;
   __shared__ double t[64][65];
   const double* __restrict__ n = a.n.get();
@@ -99,6 +100,9 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   };
   if (it0 < it1) prefetch(it0);
   __syncthreads();
+  // launched as a programmatic dependent of the transpose of n: everything above (twiddle table,
+  // first operand prefetch) overlapped it; ng is read only after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   double nl[16];
   double2 base = czero();
   int cur_o = -1;
@@ -134,6 +138,10 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
+    if (item + a.pfd + 1 < it1 && lane == 0 && !(a.dbg & 128)) {
+      const int o2 = (item + a.pfd + 1) / gcount, ub2 = g0 + (item + a.pfd + 1) % gcount;
+      prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
+    }
     {
       warp_fft1024_a<-1, true>(v, tw, lane);
       // the previous item's tile goes out while step A runs (one instruction stream, so the
@@ -168,30 +176,64 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
 }
 
-// Column pass with TMA tile stores: as k_colt, but the finished tile is laid out in TMA's 128-byte
-// swizzle (chunk c of row i at c ^ (i & 7)) and written back by four asynchronous bulk tensor
-// stores issued by one thread, which drain while the next item's operands arrive and its step A
-// runs. The exchange keeps its own swizzle (tile_idx), so a barrier separates the last exchange
-// read from the first output write; the tile is reused only after the bulk stores have read it.
-__device__ __forceinline__ int tma_idx(int i, int c) { return i * 8 + (c ^ (i & 7)); }
+// Column pass with TMA tile stores and no CTA-wide barrier in the loop (warps drift apart, so
+// one warp's memory phase overlaps another's transform). As k_colt, an item is (column octet,
+// rank) and the 8 warps' outputs form a 1024 x 8 tile of 16-byte chunks written back as full
+// 128-byte Y row lines — here by four bulk tensor stores (TMA, 128-byte swizzle) issued by the
+// last warp to finish its output, so the copy-out runs on the TMA engine.
+// Every access to the tile uses the TMA swizzle: warp w owns chunk w ^ (r & 7) of physical row
+// r. Output entry i sits at row i; the exchange runs through rows r(i) = i ^ ((i >> 5) & 7), which
+// keeps both exchange patterns (i = 32k + lane, i = 32 lane + l) conflict-free. Since a warp only
+// ever touches its own chunk of each row, the exchange and the output need no barrier between
+// warps; the only cross-warp dependencies are "all 8 outputs written" (shared counter, the 8th
+// warp issues the stores) and "the previous tile has been read by the TMA" (mbarrier the issuing
+// thread arrives on once its bulk group's reads completed), waited for before each exchange.
+// Moment sums are written per warp (8 partial blocks per octet).
+__device__ __forceinline__ int xch_idx(int i, int w) {
+  const int r = i ^ ((i >> 5) & 7);
+  return r * 8 + (w ^ (r & 7));
+}
+__device__ __forceinline__ int out_idx(int i, int w) { return i * 8 + (w ^ (i & 7)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+          (unsigned)__cvta_generic_to_shared(b)),
+      "r"(parity) : "memory");
+}
 __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, const __grid_constant__ CUtensorMap ytm) {
   extern __shared__ double2 smem_raw[];
   double2* T = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
   double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
-  __shared__ double red[8][4];
   __shared__ double2 tk[8][32];
+  __shared__ uint64_t empty_bar;   // phase j completes when the bulk stores of local item j read T
+  __shared__ unsigned done_cnt;    // warps that finished their output, over all items
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int items = (kW_N2 / 8) * gcount;
   const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
   const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
   for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
+  if (tid == 0) {
+    mbar_init(&empty_bar, 1);
+    done_cnt = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   double2* Sw = S + w * kW_H;
   auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * w + (o & 1); };
-  auto prefetch = [&](int item) {
+  auto src_of = [&](int item) {
     const int o = item / gcount, ub = g0 + item % gcount;
-    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
+    return a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
+  };
+  auto prefetch = [&](int item) {
+    const double2* src = src_of(item);
 #pragma unroll
     for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
     cp_async_commit();
@@ -200,10 +242,12 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
   const uint64_t tmp = reinterpret_cast<uint64_t>(&ytm);
   if (it0 < it1) prefetch(it0);
   __syncthreads();
+  bool issuer = false;  // this thread issued the bulk stores of the previous item
   double nl[16];
   double2 base = czero();
   int cur_o = -1;
   for (int item = it0; item < it1; ++item) {
+    const int j = item - it0;
     const int o = item / gcount, g = item % gcount, ub = g0 + g;
     const int n2 = col_of(o);
     if (o != cur_o) {
@@ -211,6 +255,7 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
 #pragma unroll
       for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
       base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
+      __syncwarp();
       tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
     }
     cp_async_wait_all();
@@ -235,27 +280,47 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
-    warp_fft1024_a<-1, true>(v, tw, lane);
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();  // the previous tile has been read by its bulk stores
-    warp_fft1024_tb<-1>(v, T, w, lane);
-    __syncthreads();  // every exchange read is done before the output writes (other swizzle)
-#pragma unroll
-    for (int k = 0; k < 32; ++k) T[tma_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
+    if (item + a.pfd + 1 < it1 && lane == 0) prefetch_l2(src_of(item + a.pfd + 1), kW_H * sizeof(double2));
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     s3 = warp_sum(s3);
-    if (lane == 0) {
-      red[w][0] = s0;
-      red[w][1] = s1;
-      red[w][2] = s2;
-      red[w][3] = s3;
+    if (lane < 4) {
+      const double t = lane == 0 ? s0 : lane == 1 ? s1 : lane == 2 ? s2 : s3;
+      a.partials[((int64_t)ub * (kW_N2 / 8) * 8 + o * 8 + w) * 4 + lane] = t;
     }
+    warp_fft1024_a<-1, true>(v, tw, lane);
+    if (j > 0) {
+      // the previous tile must have been read by its bulk stores before the exchange reuses it
+      if (issuer) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&empty_bar);
+        issuer = false;
+      }
+      mbar_wait(&empty_bar, (unsigned)((j - 1) & 1));
+    }
+#pragma unroll
+    for (int k = 0; k < 32; ++k) T[xch_idx(32 * k + lane, w)] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int l = 0; l < 32; ++l) v[l] = T[xch_idx(32 * lane + l, w)];
+    Dft<32, -1>::run(v);
+    __syncwarp();
+    // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
+#pragma unroll
+    for (int k = 0; k < 32; ++k) T[out_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
+    // make this warp's writes visible to the TMA (async proxy), then count the warp in
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0 && !(a.dbg & 2)) {
-      // rows g * 1024 + 256 b .. +255, doubles 2 * slot0 .. +15 of Y viewed as [rows][4096]
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) {
+      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(prev) : "r"((unsigned)__cvta_generic_to_shared(&done_cnt)) : "memory");
+    }
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if ((prev & 7) == 7 && lane == 0 && !(a.dbg & 2)) {
+      // the 8th warp: every output of this item is in T
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       const int x = 2 * ((o & 1) * (kW_N2 / 2) + 8 * (o >> 1));
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
@@ -264,15 +329,14 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
                      ::"l"(tmp), "r"(x), "r"(yrow), "r"(tsm + b * 256 * 128) : "memory");
       }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    if (tid < 4) {
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) t += red[q][tid];
-      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
+      issuer = true;
+    } else if ((prev & 7) == 7 && lane == 0) {
+      issuer = true;  // (stores disabled for experiments) still release the tile
     }
   }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (issuer) {
+    if (!(a.dbg & 2)) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
 }
 
 // Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
@@ -312,21 +376,35 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     double2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j];
+    // rank g's samples are loaded while rank g-1's split product runs (v is free once the
+    // transform has been parked in Xw), so the HBM latency hides behind the product phase
+    double2 v[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) v[r] = rsrc[lane + 32 * r];
     for (int g = 0; g < gcount; ++g) {
       const double wt = a.uniq_weight[g0 + g];
-      const double2* __restrict__ src = rsrc + (int64_t)g * P;
-      double2 v[32];
-      if (!(a.dbg & 64)) {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
-      } else {
-#pragma unroll
-        for (int r = 0; r < 32; ++r) v[r] = make_double2(r, lane);
+      if (lane == 0 && !(a.dbg & 128)) {
+        // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
+        // L2, so the register loads of the next items hit L2
+        int gn = g + a.pfd, k1n = k1;
+        if (gn >= gcount) {
+          gn -= gcount;
+          k1n += 2 * gridDim.x;
+        }
+        if (k1n < nrows) {
+          const int rown = rho == 0 ? k1n : (n1 - k1n) & (n1 - 1);
+          prefetch_l2(a.y + (int64_t)gn * P + (int64_t)rown * kW_N2 + h * (kW_N2 / 2), 1024 * sizeof(double2));
+        }
       }
       if (!(a.dbg & 16)) warp_fft1024<-1, false>(v, Xw, tw, lane);
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
+      if (g + 1 < gcount) {
+        const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * P;
+#pragma unroll
+        for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
+      }
       bar_sync(bar, 128);
       if (!(a.dbg & 32))
 #pragma unroll
@@ -394,10 +472,24 @@ __global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
 // (rhs.cpp:24-46, 162-168, 170-210, 227-229). A pure stream over U (R x M) at full occupancy;
 // it runs on the SMs the last row launch leaves free, beside the row transforms.
 __global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
+  extern __shared__ double dsm[];  // 4 rf moment totals, 2 r gains, r + 2 scalars
   if (!(a.skip && *a.skip)) {
     const double* __restrict__ n = a.n.get();
     RhsArgs b = a;
     b.flags = a.flags & ~T_BIRTH;
+    // w_a and the shattering gains from the column pass' moment partials, reduced by every CTA
+    // in the same fixed order (bitwise identical copies; nothing on the critical path)
+    {
+      double* tot = dsm;
+      double* sh = tot + 4 * a.rf;
+      b.scalars = sh + 2 * a.r;
+      reduce_partials_wide(a, a.nblk_colfwd, tot);
+      __syncthreads();
+      finalize_scalars_cta(b, tot, n[0], sh);
+      __syncthreads();
+      if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < a.r + 2; i += blockDim.x) a.scalars[i] = b.scalars[i];
+    }
     const bool rs = (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) != 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if ((a.m & 1) == 0) {
@@ -408,7 +500,7 @@ __global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
         double r[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         if (rs) {
           for (int ra = 0; ra < a.r; ++ra) {
-            const double w = __ldg(a.scalars + ra);
+            const double w = b.scalars[ra];
             const double* __restrict__ ur = a.ut + (int64_t)ra * a.m;
             double2 u[4];
 #pragma unroll
@@ -546,10 +638,12 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
                          void* mk) {
   RhsArgs a = a0;
   if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);  // experiment switches (tools/ab.sh)
+  a.pfd = 1;                                                 // L2 prefetch distance (items)
+  if (const char* e = getenv("AGK_PFD")) a.pfd = atoi(e);
   const int nsm = p.nsm > 0 ? p.nsm : 148;
-  a.nblk_colfwd = kW_N2 / 8;
   k_transpose_n<<<(kW_H / 64) * (kW_N2 / 64), 256, 0, s>>>(a);
   if (mark) mark(mk, K_TRANSPOSE, s);
+  a.nblk_colfwd = kW_N2 / 8;
   const int rows = kW_N1 / 2 + 1;
   // 2 row pairs per half; the SMs left over run D
   const int per = (rows + 2 * nsm - 1) / (2 * nsm);
@@ -558,11 +652,24 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
-    static const bool tma = getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 1;  // measured slower
+    static const bool tma = getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 1;  // opt-in: measured slower
     if (tma && p.ytmap_ok) {
+      a.nblk_colfwd = kW_N2;  // per-warp moment partials
       k_colm<<<items < nsm ? items : nsm, 256, smem_colm(), s>>>(a, g0, gc, p.ytmap);
     } else {
-      k_colt<<<items < nsm ? items : nsm, 256, smem_colt(), s>>>(a, g0, gc);
+      // programmatic dependent of the transpose (first group) or of the previous row launch
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(items < nsm ? items : nsm);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = smem_colt();
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = (mark || g0 > 0) ? 0 : 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&cfg, k_colt, a, g0, gc);
+      if (e != cudaSuccess) return e;
     }
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
@@ -570,7 +677,6 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
       if (mark) mark(mk, K_ROW, s);
       continue;
     }
-    k_scalars_w<<<1, 256, 2 * a.r * sizeof(double), s>>>(a);  // every column partial exists
     k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
     if (mark) mark(mk, K_ROW, s);
     // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
@@ -579,6 +685,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
     cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
