@@ -316,17 +316,54 @@ __device__ __forceinline__ void block_fft(double2 (&v)[E], double2* sm, int j, c
 //   exchange through the warp's region xs (32 rows x 33, conflict-free both ways);
 //   step B: DFT_32 over l in registers.
 constexpr int kXS = 32 * 33;  // double2 entries of a warp exchange region
-template <int SIGN, bool HALFZERO>
+// Step-A twiddles v[k] *= W_1024^{SIGN lane k}, k = 1..31, from 4 table entries: four chains
+// t_{j+4m} = t_j (W^{4 lane})^m, at most 7 roundings each (~1e-15 relative), in place of 31
+// shared-memory loads on the transform's critical path.
+template <int SIGN>
+__device__ __forceinline__ void twiddle_a_rec(double2 (&v)[32], const double2* tw, int lane) {
+  double2 t[4], w4;
+  t[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int j = 1; j < 4; ++j) t[j] = tw[j * 32 + lane];
+  w4 = tw[4 * 32 + lane];
+  if (SIGN > 0) {
+#pragma unroll
+    for (int j = 1; j < 4; ++j) t[j] = cconj(t[j]);
+    w4 = cconj(w4);
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 4 * m + j;
+      if (m == 0 && j == 0) continue;
+      if (m == 1 && j == 0) {
+        v[k] = cmul(v[k], w4);
+        continue;
+      }
+      v[k] = cmul(v[k], t[j]);
+    }
+    if (m < 7) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = (m == 0 && j == 0) ? w4 : cmul(t[j], w4);
+    }
+  }
+}
+template <int SIGN, bool HALFZERO, bool REC = false>
 __device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, const double2* tw, int lane) {
   if constexpr (HALFZERO) {
     dft_halfzero<32, SIGN>(v);
   } else {
     Dft<32, SIGN>::run(v);
   }
+  if constexpr (REC) {
+    twiddle_a_rec<SIGN>(v, tw, lane);
+  } else {
 #pragma unroll
-  for (int k = 1; k < 32; ++k) {
-    const double2 w = tw[k * 32 + lane];
-    v[k] = cmul(v[k], SIGN < 0 ? w : cconj(w));
+    for (int k = 1; k < 32; ++k) {
+      const double2 w = tw[k * 32 + lane];
+      v[k] = cmul(v[k], SIGN < 0 ? w : cconj(w));
+    }
   }
   __syncwarp();
 #pragma unroll
@@ -343,17 +380,21 @@ __device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, cons
 // one chunk per row, eight warps can share one tile without synchronising.
 __device__ __forceinline__ int tile_idx(int i, int w) { return i * 8 + (w ^ ((i ^ (i >> 5)) & 7)); }
 // step A alone (registers + twiddle table): the caller may interleave other work before step B
-template <int SIGN, bool HALFZERO>
+template <int SIGN, bool HALFZERO, bool REC = false>
 __device__ __forceinline__ void warp_fft1024_a(double2 (&v)[32], const double2* tw, int lane) {
   if constexpr (HALFZERO) {
     dft_halfzero<32, SIGN>(v);
   } else {
     Dft<32, SIGN>::run(v);
   }
+  if constexpr (REC) {
+    twiddle_a_rec<SIGN>(v, tw, lane);
+  } else {
 #pragma unroll
-  for (int k = 1; k < 32; ++k) {
-    const double2 t = tw[k * 32 + lane];
-    v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
+    for (int k = 1; k < 32; ++k) {
+      const double2 t = tw[k * 32 + lane];
+      v[k] = cmul(v[k], SIGN < 0 ? t : cconj(t));
+    }
   }
 }
 // L1-resident read-only loads (twiddle tables read from global memory) and L1-bypassing

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
-      warp_fft1024_a<-1, true>(v, tw, lane);
+      warp_fft1024_a<-1, true>(v, tw, lane);  // (table twiddles: the recurrence measured slower here)
       // the previous item's tile goes out while step A runs (one instruction stream, so the
       // stores interleave with the transform); the first item stores its own (not yet written)
       // tile to its own destination, which its real store overwrites later in program order
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           prefetch_l2(a.y + (int64_t)gn * P + (int64_t)rown * kW_N2 + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
-      if (!(a.dbg & 16)) warp_fft1024<-1, false>(v, Xw, tw, lane);
+      if (!(a.dbg & 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
@@ -406,6 +406,9 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       }
       bar_sync(bar, 128);
+      // W_2048^ht and W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1))
+      const double2 wb1 = twh[ht];
+      const double2 wb2 = k1 == 0 ? make_double2(-wb1.x, wb1.y) : make_double2(-twh[ht + 1].x, twh[ht + 1].y);
       if (!(a.dbg & 32))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -415,7 +418,10 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
         const double sa = (k1 == 0 && qp == 0) ? 1.0 : -1.0;
         const double2 e1 = Xh[qp], o1 = Xh[kXR + qp];
         const double2 e2 = Xh[2 * kXR + m], o2 = Xh[3 * kXR + m];
-        const double2 t1 = cmul(o1, twh[qp]), t2 = cmul(o2, twh[m]);
+        // W_2048^qp = W_2048^ht W_16^j and W_2048^m = W_2048^(m mod 128 base) W_16^-j: two table
+        // entries per thread, the W_16 factors are compile-time constants
+        const double2 t1 = mul_w16<-1>(cmul(o1, wb1), j);
+        const double2 t2 = (k1 == 0 && qp == 0) ? o2 : mul_w16<+1>(cmul(o2, wb2), j);
         const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
         const double2 pa = make_double2(e2.x + sa * t2.x, e2.y + sa * t2.y);
         const double2 pb = make_double2(e2.x - sa * t2.x, e2.y - sa * t2.y);
