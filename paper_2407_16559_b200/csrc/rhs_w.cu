@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
-      warp_fft1024_a<-1, true>(v, tw, lane);  // (table twiddles: the recurrence measured slower here)
+      warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
       // the previous item's tile goes out while step A runs (one instruction stream, so the
       // stores interleave with the transform); the first item stores its own (not yet written)
       // tile to its own destination, which its real store overwrites later in program order
@@ -153,8 +153,26 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     }
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
+    if (!(a.dbg & 2048)) {
+      // four chains t_{j+4m} = (base W_P^{32 n2 j}) (W_P^{128 n2})^m: 5 shared loads instead
+      // of 32 on the critical path, at most 7 roundings per factor
+      double2 t[4];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) T[tile_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
+      for (int j = 0; j < 4; ++j) t[j] = cmul(base, tk[w][j]);
+      const double2 st = tk[w][4];
+#pragma unroll
+      for (int mm = 0; mm < 8; ++mm) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) T[tile_idx(lane + 32 * (4 * mm + j), w)] = cmul(v[4 * mm + j], t[j]);
+        if (mm < 7) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) t[j] = cmul(t[j], st);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 32; ++k) T[tile_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
+    }
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
