@@ -98,6 +98,45 @@ struct RhsPlan {
 // kernel classes for per-launch timing
 enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANSPOSE = 4, K_DVEC = 5, K_ROW_INV = 6, K_DENSE_ROWS = 7, K_DENSE_BIRTH = 8 };
 
+// Programmatic dependent launch (PDL) along the chain of kernels of one RHS and of one RK trial:
+// a kernel launched with pdl = true is scheduled while its predecessor drains, runs only a
+// prologue that touches immutable data (twiddle tables, kernel factors) and shared memory, then
+// pdl_entry()/griddepcontrol.wait before anything written by earlier launches, and triggers its
+// own dependents only after that wait — so a dependent overlaps its immediate predecessor only.
+// AGK_PDL=0 turns it off (ordinary stream serialisation); per-kernel timing marks also do.
+bool pdl_enabled();
+int pdl_mask();  // AGK_PDLMASK experiment bits (default all)
+#ifndef AGK_CK
+#define AGK_CK(...)                   \
+  do {                                \
+    cudaError_t e_ = (__VA_ARGS__);   \
+    if (e_ != cudaSuccess) return e_; \
+  } while (0)
+#endif
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_wait();
+  pdl_trigger();
+}
+#endif
+
 // host-side launchers (rhs.cu)
 void rhs_make_plan(int64_t m, int rf, RhsPlan* plan);
 cudaError_t rhs_launch(const RhsPlan& plan, const RhsArgs& a, cudaStream_t s);

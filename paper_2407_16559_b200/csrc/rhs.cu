@@ -43,6 +43,7 @@ struct SmallCfg {
 
 template <int P>
 __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
+  pdl_entry();
   using CF = SmallCfg<P>;
   constexpr int E = CF::E, T = CF::T, NT = CF::NT;
   using PL = typename CF::PL;
@@ -172,6 +173,7 @@ struct Cfg {
 
 template <int N1, int E1, int C>
 __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int gcount) {
+  pdl_entry();
   using PL = FftPlan<N1, E1>;
   constexpr int T1 = N1 / E1, NT = C * T1, H = E1 / 2;
   constexpr int RG = PL::template smem<kNoPad>();
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
 
 template <int N2, int E2, bool STAGE, int MINB>
 __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
+  pdl_entry();
   using PL = FftPlan<N2, E2>;
   constexpr int T2 = N2 / E2, NT = 2 * T2, Q = E2 / 2;
   extern __shared__ double2 smem[];
@@ -340,6 +343,7 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
 
 template <int N1, int E1, int CP>
 __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
+  pdl_entry();
   using PL = FftPlan<N1, E1>;
   constexpr int T1 = N1 / E1;
   constexpr int RG = PL::template smem<kNoPad>();
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
 // ------------------------------------------------------------------ injected fakes
 
 __global__ void k_fake(int kind, double param, VecRef nref, double* out, int64_t m, const int* skip) {
+  pdl_entry();
   if (skip && *skip) return;
   const double* n = nref.get();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
@@ -400,7 +405,7 @@ cudaError_t fake_rhs_launch(int kind, double param, VecRef n, double* out, int64
   const int threads = 256;
   int blocks = (int)((m + threads - 1) / threads);
   if (blocks > 4 * 148) blocks = 4 * 148;
-  k_fake<<<blocks, threads, 0, s>>>(kind, param, n, out, m, skip);
+  AGK_CK(launch_k(k_fake, blocks, threads, 0, s, pdl_enabled(), kind, param, n, out, m, skip));
   return cudaGetLastError();
 }
 
@@ -435,7 +440,7 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   const int ngroups = (rf + g - 1) / g;
   const char* fe = getenv("AGK_FAST");
   p->fast = (L == 21) && !(fe && atoi(fe) == 0);
-  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);
+  p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);  // fast: + transpose, dvec
   p->nsm = 148;
   p->dense = 0;
   p->ytmap_ok = 0;
@@ -463,9 +468,21 @@ static void mark(Marks* mk, int cls, cudaStream_t s) {
 }
 static void mark_cb(void* mk, int cls, cudaStream_t s) { mark(static_cast<Marks*>(mk), cls, s); }
 
+bool pdl_enabled() {
+  static const bool on = !(getenv("AGK_PDL") && atoi(getenv("AGK_PDL")) == 0);
+  return on;
+}
+int pdl_mask() {
+  // measured per edge (tools/ab.sh): on for the transpose -> column pass, -> inverse column
+  // pass and the RK-trial chain, and for the four-step path at P = 2^13; off for column -> row
+  // passes and the mid-size four-step path, where the early-placed dependent grid was slower
+  static const int m = getenv("AGK_PDLMASK") ? atoi(getenv("AGK_PDLMASK")) : (2 | 8 | 16 | 64);
+  return m;
+}
+
 template <int P>
 static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s, Marks* mk) {
-  k_small<P><<<1, SmallCfg<P>::NT, SmallCfg<P>::SMEM_BYTES, s>>>(a);
+  AGK_CK(launch_k(k_small<P>, 1, SmallCfg<P>::NT, SmallCfg<P>::SMEM_BYTES, s, !mk && pdl_enabled() && (pdl_mask() & 32), a));
   mark(mk, K_SMALL, s);
   return cudaGetLastError();
 }
@@ -475,14 +492,16 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
   RhsArgs a = a0;
   a.nblk_colfwd = CF::N2 / CF::C;
   const size_t sm1 = CF::SM_COLFWD, sm2 = CF::SM_ROW, sm3 = CF::SM_COLINV;
+  const bool pdl = !mk && pdl_enabled() && (pdl_mask() & (CF::N1 * CF::N2 <= 8192 ? 64 : 32));
   for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
-    k_col_fwd<CF::N1, CF::E1, CF::C><<<CF::N2 / CF::C, CF::C * CF::T1, sm1, s>>>(a, g0, gc);
+    AGK_CK(launch_k(k_col_fwd<CF::N1, CF::E1, CF::C>, CF::N2 / CF::C, CF::C * CF::T1, sm1, s, pdl, a, g0, gc));
     mark(mk, K_COL_FWD, s);
-    k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB><<<CF::N1 / 2 + 1, 2 * CF::T2, sm2, s>>>(a, g0, gc, g0 == 0, g0 + gc >= a.rf);
+    AGK_CK(launch_k(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, CF::N1 / 2 + 1, 2 * CF::T2, sm2, s, pdl, a, g0,
+                    gc, (int)(g0 == 0), (int)(g0 + gc >= a.rf)));
     mark(mk, K_ROW, s);
   }
-  k_col_inv<CF::N1, CF::E1, CF::CP><<<CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s>>>(a);
+  AGK_CK(launch_k(k_col_inv<CF::N1, CF::E1, CF::CP>, CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s, pdl, a));
   mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }

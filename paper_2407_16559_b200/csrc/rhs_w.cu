@@ -38,7 +38,7 @@ __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 64 x 64 tiles, 16 elements
 // per thread in flight, 256-byte coalesced rows both ways.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the column pass' prologue may start
+  pdl_entry();  // then the column pass' prologue may start
   if (a.skip && *a.skip) return;
   __shared__ double t[64][65];
   const double* __restrict__ n = a.n.get();
@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
   __shared__ double red[8][4];
   __shared__ double2 tk[8][32];    // four-step factors W_P^{32 n2 k} of the warp's column
-  if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int items = (kW_N2 / 8) * gcount;
   const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
@@ -102,7 +101,11 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   __syncthreads();
   // launched as a programmatic dependent of the transpose of n: everything above (twiddle table,
   // first operand prefetch) overlapped it; ng is read only after it completed
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_entry();
+  if (a.skip && *a.skip) {
+    cp_async_wait_all();
+    return;
+  }
   double nl[16];
   double2 base = czero();
   int cur_o = -1;
@@ -233,7 +236,6 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
   __shared__ double2 tk[8][32];
   __shared__ uint64_t empty_bar;   // phase j completes when the bulk stores of local item j read T
   __shared__ unsigned done_cnt;    // warps that finished their output, over all items
-  if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int items = (kW_N2 / 8) * gcount;
   const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
@@ -260,6 +262,11 @@ __global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, 
   const uint64_t tmp = reinterpret_cast<uint64_t>(&ytm);
   if (it0 < it1) prefetch(it0);
   __syncthreads();
+  pdl_entry();
+  if (a.skip && *a.skip) {
+    cp_async_wait_all();
+    return;
+  }
   bool issuer = false;  // this thread issued the bulk stores of the previous item
   double nl[16];
   double2 base = czero();
@@ -374,7 +381,8 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
   double2* twh = tw + 1024;        // W_2048^j, j < 1024
   __shared__ double2 tkk[8][32];
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // after the column pass completed: k_dvec (dependent) reads its moment partials
+  pdl_entry();
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
             h = hw & 1, ht = tid & 127, bar = 1 + hf;
@@ -481,17 +489,6 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   }
 }
 
-// w_a, pair and monomer gains from the column pass' partials (one CTA, fixed order)
-__global__ void __launch_bounds__(256) k_scalars_w(RhsArgs a) {
-  extern __shared__ double sh[];  // 2 r
-  if (a.skip && *a.skip) return;
-  const double n0 = a.n.get()[0];
-  double* tot = a.scalars + a.r + 2;
-  reduce_partials_wide(a, a.nblk_colfwd, tot);
-  __syncthreads();
-  finalize_scalars_cta(a, tot, n0, sh);
-}
-
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
 // (rhs.cpp:24-46, 162-168, 170-210, 227-229). A pure stream over U (R x M) at full occupancy;
 // it runs on the SMs the last row launch leaves free, beside the row transforms.
@@ -556,7 +553,7 @@ __global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
   }
   // launched as a programmatic dependent of the row kernel: do not complete before it does, so
   // the launches after this one see the row results (no-op for an ordinary launch)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_entry();
 }
 
 // Inverse column pass: two real columns per complex 1024-pt inverse FFT, then S = birth + D.
@@ -569,6 +566,7 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   constexpr int GS = 2 * kCW + 1, GROWS = kW_N1 / 2 + 1;
   double2* tw = X + GROWS * GS;
   double* dv = reinterpret_cast<double*>(tw + 1024);  // [512][2 kCW] D values of the output tile
+  pdl_entry();
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
@@ -655,9 +653,10 @@ cudaError_t rhs_w_set_smem_limits() {
   return cudaSuccess;
 }
 
-// One RHS: transpose of n | per rank group, column pass | row pass (the last one also runs the inverse row
-// transform; the scalars go just before it and D beside it) | inverse column pass with the
-// epilogue. 6 launches for <= 16 unique ranks (the plan's `launches`).
+// One RHS: transpose of n | per rank group, column pass | row pass (the last one also runs the
+// inverse row transform, with D computed beside it on the SMs the row grid leaves free) | inverse
+// column pass with the epilogue. 5 launches for <= 16 unique ranks (the plan's `launches`), each a
+// programmatic dependent of the one before (pdl_entry in every kernel; off under timing marks).
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
   RhsArgs a = a0;
@@ -665,7 +664,8 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
   a.pfd = 1;                                                 // L2 prefetch distance (items)
   if (const char* e = getenv("AGK_PFD")) a.pfd = atoi(e);
   const int nsm = p.nsm > 0 ? p.nsm : 148;
-  k_transpose_n<<<(kW_H / 64) * (kW_N2 / 64), 256, 0, s>>>(a);
+  const bool pdl = !mark && pdl_enabled();
+  AGK_CK(launch_k(k_transpose_n, (kW_H / 64) * (kW_N2 / 64), 256, 0, s, pdl && (pdl_mask() & 1), a));
   if (mark) mark(mk, K_TRANSPOSE, s);
   a.nblk_colfwd = kW_N2 / 8;
   const int rows = kW_N1 / 2 + 1;
@@ -676,55 +676,34 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
+    const int cgrid = items < nsm ? items : nsm;
     static const bool tma = getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 1;  // opt-in: measured slower
     if (tma && p.ytmap_ok) {
       a.nblk_colfwd = kW_N2;  // per-warp moment partials
-      k_colm<<<items < nsm ? items : nsm, 256, smem_colm(), s>>>(a, g0, gc, p.ytmap);
+      AGK_CK(launch_k(k_colm, cgrid, 256, smem_colm(), s, pdl, a, g0, gc, p.ytmap));
     } else {
-      // programmatic dependent of the transpose (first group) or of the previous row launch
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(items < nsm ? items : nsm);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = smem_colt();
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = (mark || g0 > 0) ? 0 : 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      const cudaError_t e = cudaLaunchKernelEx(&cfg, k_colt, a, g0, gc);
-      if (e != cudaSuccess) return e;
+      AGK_CK(launch_k(k_colt, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     }
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
-      k_rowd<false><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
+      AGK_CK(launch_k(k_rowd<false>, rgrid, 256, smem_rowd(), s, pdl, a, g0, gc, (int)(g0 == 0)));
       if (mark) mark(mk, K_ROW, s);
       continue;
     }
-    k_rowd<true><<<rgrid, 256, smem_rowd(), s>>>(a, g0, gc, g0 == 0);
+    AGK_CK(launch_k(k_rowd<true>, rgrid, 256, smem_rowd(), s, pdl && (pdl_mask() & 4), a, g0, gc, (int)(g0 == 0)));
     if (mark) mark(mk, K_ROW, s);
-    // D on the SMs the row grid leaves free (programmatic dependent launch: k_dvec starts once
-    // every row CTA is resident and waits for the row grid before it exits)
+    // D on the SMs the row grid leaves free: k_dvec starts once every row CTA passed its wait
+    // (the column pass is complete) and waits for the row grid before it exits
     const int free = nsm - rgrid;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(8 * (free > 1 ? free : 1));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double);
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = mark ? 0 : 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_dvec, a);
-    if (e != cudaSuccess) return e;
+    AGK_CK(launch_k(k_dvec, 8 * (free > 1 ? free : 1), 256, (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double), s,
+                    !mark, a));
     if (mark) mark(mk, K_DVEC, s);
   }
   static const bool civ4 = getenv("AGK_CIV") && atoi(getenv("AGK_CIV")) == 4;
   if (civ4) {
-    k_colinvw<4><<<kW_N2 / 8, 128, smem_colinvw4(), s>>>(a);
+    AGK_CK(launch_k(k_colinvw<4>, kW_N2 / 8, 128, smem_colinvw4(), s, pdl, a));
   } else {
-    k_colinvw<8><<<kW_N2 / 16, 256, smem_colinvw(), s>>>(a);
+    AGK_CK(launch_k(k_colinvw<8>, kW_N2 / 16, 256, smem_colinvw(), s, pdl && (pdl_mask() & 8), a));
   }
   if (mark) mark(mk, K_COL_INV, s);
   return cudaGetLastError();

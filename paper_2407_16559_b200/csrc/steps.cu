@@ -73,6 +73,7 @@ __device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
 
 template <int KIND, bool RED>
 __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
+  pdl_entry();
   const double t = a.tau_mul * a.ctl->tau;
   const double* __restrict__ x = a.x.get();
   double* __restrict__ out = a.out.get();
@@ -359,6 +360,7 @@ __global__ void k_prologue(DevCtl* c, const double* mom_part, int nmom, const do
 
 __global__ void __launch_bounds__(32) k_controller(DevCtl* c, const double* part, int nblk,
                                                    cudaGraphConditionalHandle h) {
+  pdl_entry();
   // fixed-order reduction of the final pass' CTA partials
   const int lane = threadIdx.x;
   double v[RF_N];
@@ -463,6 +465,7 @@ __global__ void __launch_bounds__(32) k_controller(DevCtl* c, const double* part
 
 // Deep copies of the accepted state for the snapshot times the controller just reached.
 __global__ void k_snap_copy(const DevCtl* c, const double* state, int64_t m) {
+  pdl_entry();
   const int from = c->snap_from, to = c->snap_to;
   if (to <= from || !c->snap_buf) return;
   const double* x = state + c->cur * m;
@@ -480,15 +483,10 @@ int red_blocks_for(int64_t m) {
   return (int)b;
 }
 
-#define AGK_CK(...)                        \
-  do {                                     \
-    cudaError_t e_ = (__VA_ARGS__);        \
-    if (e_ != cudaSuccess) return e_;      \
-  } while (0)
 
 template <int KIND, bool RED>
 static cudaError_t comb(CombArgs a, int nblk, cudaStream_t s) {
-  k_comb<KIND, RED><<<nblk, kRedThreads, 0, s>>>(a);
+  AGK_CK(launch_k(k_comb<KIND, RED>, nblk, kRedThreads, 0, s, pdl_enabled() && (pdl_mask() & 16), a));
   return cudaGetLastError();
 }
 
@@ -636,8 +634,8 @@ cudaError_t build_step_graph(int body, int stepper, const RhsEnqueue& rhs, const
       AGK_CK(step(plain(b.mid), K[6], true, nullptr, 0.5, nullptr, true, b.full));
     }
   }
-  k_controller<<<1, 32, 0, s>>>(ctl, b.red, nb, h);
-  k_snap_copy<<<nb, kRedThreads, 0, s>>>(ctl, b.state, m);
+  AGK_CK(launch_k(k_controller, 1, 32, 0, s, pdl_enabled() && (pdl_mask() & 16), ctl, (const double*)b.red, nb, h));
+  AGK_CK(launch_k(k_snap_copy, nb, kRedThreads, 0, s, pdl_enabled() && (pdl_mask() & 16), (const DevCtl*)ctl, (const double*)b.state, m));
   nk += 2;
   AGK_CK(cudaGetLastError());
   cudaGraph_t bg = nullptr;
