@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "agk_oracle.h"
+#include "aggkin/analysis.hpp"
 #include "aggkin/bench.hpp"
 #include "aggkin/config.hpp"
 #include "aggkin/report_io.hpp"
@@ -294,3 +295,50 @@ extern "C" int ref_write_bench_outputs(const int* schemes, size_t ns, const int*
   }
 }
 
+
+// Config text -> serialize_config(parse_config_text(text)) (config.cpp:131-438), or the error
+// message: returns 0 (serialized), 1 (ConfigError), 2 (other exception); out is NUL-terminated.
+extern "C" int ref_parse_config(const char* text, char* out, size_t cap) {
+  std::string s;
+  int rc = 0;
+  try {
+    s = serialize_config(parse_config_text(text));
+  } catch (const ConfigError& e) {
+    s = e.what();
+    rc = 1;
+  } catch (const std::exception& e) {
+    s = e.what();
+    rc = 2;
+  }
+  const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+  std::memcpy(out, s.data(), n);
+  out[n] = '\0';
+  return rc;
+}
+
+// kernel_entry (kernels.cpp:36-57); variant 0 constant, 1 brownian, 2 free_molecular, 3 factors
+extern "C" int ref_kernel_entry(int variant, double alpha, size_t i, size_t j, double* out) try {
+  KernelSpec spec;
+  spec.variant = static_cast<KernelVariant>(variant);
+  spec.alpha = alpha;
+  *out = kernel_entry(spec, i, j);
+  return 0;
+} catch (const std::exception&) {
+  return -1;
+}
+
+// fit_power_law / fit_cutoff (analysis.cpp:59-75): res = {beta, k_lo, k_hi, rms, used, excluded}
+extern "C" int ref_fit(const double* n, size_t m, double lam, int cutoff, size_t k_lo, size_t k_hi,
+                       double* res) try {
+  const std::span<const double> s(n, m);
+  const SlopeFit f = cutoff ? fit_cutoff(s, lam, k_lo, k_hi) : fit_power_law(s, k_lo, k_hi);
+  res[0] = f.beta;
+  res[1] = (double)f.k_lo;
+  res[2] = (double)f.k_hi;
+  res[3] = f.residual_rms;
+  res[4] = (double)f.points_used;
+  res[5] = (double)f.points_excluded;
+  return 0;
+} catch (const std::exception&) {
+  return -1;
+}
