@@ -194,7 +194,7 @@ def test_run_text_matches_oracle(agk, oracle_port, text):
     want = oracle_port.run(om, sim.initial, O.Control(stepper=c.stepper, mode=c.mode, tau=c.tau, tol=c.tol),
                            sim.t_end, snapshot_times=list(sim.snapshot_times), record=sim.record,
                            record_interval=sim.record_interval, records_capacity=100000)
-    assert got["termination"] == want["termination"]
+    assert got["termination"] == ("completed", "aborted")[want["termination"]]
     assert got["total_accepted"] == want["total_accepted"]
     assert got["total_rejects"] == want["total_rejects"]
     assert got["total_rhs_evals"] == want["total_rhs_evals"]
