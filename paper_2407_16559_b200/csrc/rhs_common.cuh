@@ -198,6 +198,14 @@ __device__ __forceinline__ double2 split_product(double2 z, double2 zp) {
   return make_double2(ar * br - ai * bi, ar * bi + ai * br);
 }
 
+// acc += w4 * A*B for the bin pair (z, zp) as split_product, with 4 A*B = -i (z + conj zp)(z - conj zp)
+// formed directly (the factors 1/2 are powers of two: the same roundings) and w4 = weight / 4
+__device__ __forceinline__ void split_product_acc4(double2& acc, double w4, double2 z, double2 zp) {
+  const double sx = z.x + zp.x, sy = z.y - zp.y, dx = z.x - zp.x, dy = z.y + zp.y;
+  acc.x = fma(w4, fma(sx, dy, sy * dx), acc.x);
+  acc.y = fma(w4, fma(sy, dy, -(sx * dx)), acc.y);
+}
+
 // Four-step twiddles W_P^{SIGN e} for e = e0 + r*de, r = 0..E-1, by a short recurrence from two
 // accurate two-level lookups (error ~r ulp, no per-element table loads).
 template <int SIGN>

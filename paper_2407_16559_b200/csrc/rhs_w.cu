@@ -146,13 +146,13 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
-      warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
+      if (!(a.dbg & 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
       // the previous item's tile goes out while step A runs (one instruction stream, so the
       // stores interleave with the transform); the first item stores its own (not yet written)
       // tile to its own destination, which its real store overwrites later in program order
       if (!(a.dbg & 2)) store_tile(item == it0 ? item : item - 1);
       __syncthreads();  // every warp has read the tile: it is free for the exchanges
-      warp_fft1024_tb<-1>(v, T, w, lane);
+      if (!(a.dbg & 8)) warp_fft1024_tb<-1>(v, T, w, lane);
     }
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
@@ -557,8 +557,22 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     double2 v[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) v[r] = rsrc[lane + 32 * r];
+    // the radix-2 twiddles of this thread's bins, the same for every rank: W_2048^q' for q' = ht +
+    // 128 j (row k1) and, with the combination's sign folded in, -W_2048^-m' for the partner bins
+    // of row N1-k1 (m' = 1023 - q', or N2 - q for row 0, whose bin 0 pairs with itself unrotated)
+    double2 tw1[8], tw2[8];
+    {
+      const double2 wb1 = twh[ht];
+      // W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1)), negated
+      const double2 wb2 = k1 == 0 ? make_double2(wb1.x, -wb1.y) : make_double2(twh[ht + 1].x, -twh[ht + 1].y);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        tw1[j] = mul_w16<-1>(wb1, j);
+        tw2[j] = (k1 == 0 && ht == 0 && j == 0) ? make_double2(1.0, 0.0) : mul_w16<+1>(wb2, j);
+      }
+    }
     for (int g = 0; g < gcount; ++g) {
-      const double wt = a.uniq_weight[g0 + g];
+      const double wq = 0.25 * a.uniq_weight[g0 + g];
       if (lane == 0 && !(a.dbg & 128)) {
         // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
         // L2, so the register loads of the next items hit L2
@@ -576,36 +590,25 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
-      if (g + 1 < gcount) {
+      if (g + 1 < gcount && !(a.dbg & 64)) {
         const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * P;
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       }
       bar_sync(bar, 128);
-      // W_2048^ht and W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1))
-      const double2 wb1 = twh[ht];
-      const double2 wb2 = k1 == 0 ? make_double2(-wb1.x, wb1.y) : make_double2(-twh[ht + 1].x, twh[ht + 1].y);
       if (!(a.dbg & 32))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int qp = ht + 128 * j;
         // partner bins of q' and q' + 1024 in row N1-k1 (row 0 pairs with itself at N2 - q)
         const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
-        const double sa = (k1 == 0 && qp == 0) ? 1.0 : -1.0;
         const double2 e1 = Xh[qp], o1 = Xh[kXR + qp];
         const double2 e2 = Xh[2 * kXR + m], o2 = Xh[3 * kXR + m];
-        // W_2048^qp = W_2048^ht W_16^j and W_2048^m = W_2048^(m mod 128 base) W_16^-j: two table
-        // entries per thread, the W_16 factors are compile-time constants
-        const double2 t1 = mul_w16<-1>(cmul(o1, wb1), j);
-        const double2 t2 = (k1 == 0 && qp == 0) ? o2 : mul_w16<+1>(cmul(o2, wb2), j);
+        const double2 t1 = cmul(o1, tw1[j]), t2 = cmul(o2, tw2[j]);
         const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
-        const double2 pa = make_double2(e2.x + sa * t2.x, e2.y + sa * t2.y);
-        const double2 pb = make_double2(e2.x - sa * t2.x, e2.y - sa * t2.y);
-        const double2 ra = split_product(xa, pa), rb = split_product(xb, pb);
-        acc[j].x += wt * ra.x;
-        acc[j].y += wt * ra.y;
-        acc[j + 8].x += wt * rb.x;
-        acc[j + 8].y += wt * rb.y;
+        const double2 pa = cadd(e2, t2), pb = csub(e2, t2);
+        split_product_acc4(acc[j], wq, xa, pa);
+        split_product_acc4(acc[j + 8], wq, xb, pb);
       }
       bar_sync(bar, 128);
     }
@@ -642,9 +645,9 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
 // (rhs.cpp:24-46, 162-168, 170-210, 227-229). A pure stream over U (R x M) at full occupancy;
 // it runs on the SMs the last row launch leaves free, beside the row transforms.
-__global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
+__global__ void __launch_bounds__(256, 2) k_dvec(RhsArgs a) {
   extern __shared__ double dsm[];  // 4 rf moment totals, 2 r gains, r + 2 scalars
-  if (!(a.skip && *a.skip)) {
+  if (!(a.skip && *a.skip) && !(a.dbg & 256)) {
     const double* __restrict__ n = a.n.get();
     RhsArgs b = a;
     b.flags = a.flags & ~T_BIRTH;
@@ -670,15 +673,34 @@ __global__ void __launch_bounds__(256) k_dvec(RhsArgs a) {
       for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < np; p0 += 4 * stride) {
         double r[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
         if (rs) {
-          for (int ra = 0; ra < a.r; ++ra) {
+          int64_t pk[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pk[k] = 2 * (p0 + k * stride < np ? p0 + k * stride : np - 1);  // clamped
+          int ra = 0;
+          // four ranks per step: 16 independent 16-byte loads in flight per thread (the kernel runs
+          // on the few SMs the row pass leaves free, so its memory parallelism is per thread)
+          for (; ra + 4 <= a.r; ra += 4) {
+            double2 u[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                u[q][k] = __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)(ra + q) * a.m + pk[k]));
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const double w = b.scalars[ra + q];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                r[k][0] += u[q][k].x * w;
+                r[k][1] += u[q][k].y * w;
+              }
+            }
+          }
+          for (; ra < a.r; ++ra) {
             const double w = b.scalars[ra];
-            const double* __restrict__ ur = a.ut + (int64_t)ra * a.m;
             double2 u[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int64_t p = p0 + k * stride < np ? p0 + k * stride : np - 1;  // clamped: unpredicated
-              u[k] = __ldg(reinterpret_cast<const double2*>(ur + 2 * p));
-            }
+            for (int k = 0; k < 4; ++k) u[k] = __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)ra * a.m + pk[k]));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               r[k][0] += u[k].x * w;
@@ -849,7 +871,10 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     // D on the SMs the row grid leaves free: k_dvec starts once every row CTA passed its wait
     // (the column pass is complete) and waits for the row grid before it exits
     const int free = nsm - rgrid;
-    AGK_CK(launch_k(k_dvec, 8 * (free > 1 ? free : 1), 256, (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double), s,
+    // every k_dvec CTA must be resident from the start: a CTA that finished early would otherwise
+    // hold its SM slot in the final wait for the row grid, and the rest of D would run after it
+    static const int dv_per_sm = getenv("AGK_DVPS") ? atoi(getenv("AGK_DVPS")) : 2;
+    AGK_CK(launch_k(k_dvec, dv_per_sm * (free > 1 ? free : 1), 256, (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double), s,
                     !mark, a));
     if (mark) mark(mk, K_DVEC, s);
   }
