@@ -50,6 +50,7 @@ struct agk_rhs {
   std::map<int, cudaGraphExec_t> graphs;
   std::map<int, int> graph_kernels;
   cudaGraphExec_t rhs_graph = nullptr;
+  cudaGraphExec_t rhs_graph_b = nullptr;  // kTimedBatch evaluations back to back in one graph
   const double* rhs_graph_in = nullptr;
   double* rhs_graph_out = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -661,6 +662,7 @@ void agk_rhs_destroy(agk_rhs* h) {
   cudaStreamSynchronize(h->stream);
   for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
   if (h->rhs_graph) cudaGraphExecDestroy(h->rhs_graph);
+  if (h->rhs_graph_b) cudaGraphExecDestroy(h->rhs_graph_b);
   for (void* p : h->allocs) cudaFree(p);
   if (h->ev0) cudaEventDestroy(h->ev0);
   if (h->ev1) cudaEventDestroy(h->ev1);
@@ -948,27 +950,37 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
 agk_status agk_rhs_eval_timed(agk_rhs* h, const double* n_dev, double* out_dev, int count, float* elapsed_ms) {
   if (!h || h->kind != AGK_RHS_MODEL || count < 1) return fail(h, AGK_ERR_INVALID_ARGUMENT, "bad timing request");
   DeviceGuard dg(h->device);
+  // back-to-back evaluations (BASELINE config 4 runs 1000 of them): one graph holds kTimedBatch
+  // chained evaluations, so consecutive evaluations are joined by programmatic dependent launch
+  // like the RHS evaluations inside a stepping graph, not by a graph-launch boundary
+  constexpr int kTimedBatch = 10;
   if (h->rhs_graph && (h->rhs_graph_in != n_dev || h->rhs_graph_out != out_dev)) {
     cudaGraphExecDestroy(h->rhs_graph);
     h->rhs_graph = nullptr;
+    if (h->rhs_graph_b) cudaGraphExecDestroy(h->rhs_graph_b);
+    h->rhs_graph_b = nullptr;
   }
   if (!h->rhs_graph) {
     h->rhs_graph_in = n_dev;
     h->rhs_graph_out = out_dev;
-    cudaGraph_t g;
     RhsArgs a = h->base;
     a.n = VecRef{n_dev, nullptr, 0};
     a.out = out_dev;
-    CK_H(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "capture");
-    cudaError_t e = rhs_launch(h->plan, a, h->stream);
-    cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
-    if (e != cudaSuccess) return cuda_fail(h, e, "capture rhs");
-    if (e2 != cudaSuccess) return cuda_fail(h, e2, "capture end");
-    CK_H(h, cudaGraphInstantiate(&h->rhs_graph, g, 0), "instantiate");
-    cudaGraphDestroy(g);
+    for (int b = 0; b < 2; ++b) {
+      cudaGraph_t g;
+      CK_H(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "capture");
+      cudaError_t e = cudaSuccess;
+      for (int q = 0; q < (b ? kTimedBatch : 1) && e == cudaSuccess; ++q) e = rhs_launch(h->plan, a, h->stream);
+      cudaError_t e2 = cudaStreamEndCapture(h->stream, &g);
+      if (e != cudaSuccess) return cuda_fail(h, e, "capture rhs");
+      if (e2 != cudaSuccess) return cuda_fail(h, e2, "capture end");
+      CK_H(h, cudaGraphInstantiate(b ? &h->rhs_graph_b : &h->rhs_graph, g, 0), "instantiate");
+      cudaGraphDestroy(g);
+    }
   }
   CK_H(h, cudaEventRecord(h->ev0, h->stream), "event");
-  for (int q = 0; q < count; ++q) CK_H(h, cudaGraphLaunch(h->rhs_graph, h->stream), "graph launch");
+  for (int q = 0; q < count / kTimedBatch; ++q) CK_H(h, cudaGraphLaunch(h->rhs_graph_b, h->stream), "graph launch");
+  for (int q = 0; q < count % kTimedBatch; ++q) CK_H(h, cudaGraphLaunch(h->rhs_graph, h->stream), "graph launch");
   CK_H(h, cudaEventRecord(h->ev1, h->stream), "event");
   CK_H(h, cudaEventSynchronize(h->ev1), "event sync");
   CK_H(h, cudaEventElapsedTime(elapsed_ms, h->ev0, h->ev1), "elapsed");

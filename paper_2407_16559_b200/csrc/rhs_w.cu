@@ -33,12 +33,31 @@ __device__ __forceinline__ double warp_sum(double x) {
   return x;
 }
 
+// Timeline diagnostics (AGK_DBG & 512, tools/timeline.py): per kernel class, the first CTA's
+// arrival, the first CTA's start of work (after its programmatic-dependency wait) and the last
+// CTA's exit, as %globaltimer ns, so the overlap of the chained launches can be seen in graph mode.
+__device__ unsigned long long g_timeline[8][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(const RhsArgs& a, int k, int what) {
+  if ((a.dbg & 512) && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (what < 2) atomicMin(&g_timeline[k][what], t);
+    else atomicMax(&g_timeline[k][what], t);
+  }
+}
+
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 64 x 64 tiles, 16 elements
 // per thread in flight, 256-byte coalesced rows both ways.
 __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
+  tl_mark(a, 0, 0);
   pdl_entry();  // then the column pass' prologue may start
+  tl_mark(a, 0, 1);
   if (a.skip && *a.skip) return;
   __shared__ double t[64][65];
   const double* __restrict__ n = a.n.get();
@@ -55,6 +74,7 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < 16; ++q) a.ng[(int64_t)(bx * 64 + ty + 4 * q) * kW_H + by * 64 + tx] = t[tx][ty + 4 * q];
+  tl_mark(a, 0, 2);
 }
 
 // Y layout (per rank, [k1][slot], 2048 slots per row): the row transform's first radix-2 stage
@@ -66,7 +86,9 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
 // row. Each warp's 1024-point transform exchanges through, and leaves its twiddled output in, its
 // own chunk of one swizzled 1024 x 8 tile; the CTA then writes the tile back as full 128-byte row
 // lines (4 lines per warp store). Items are rank-minor, so n is reloaded only per octet.
+template <int SV>
 __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) {
+  tl_mark(a, 1, 0);
   extern __shared__ double2 smem[];
   double2* T = smem;               // 1024 x 8 tile: exchange + output (tile_idx)
   double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
@@ -97,11 +119,23 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
     }
   };
+  // a quarter of the tile (8 lines per thread), fully unrolled: placed between pieces of step A so
+  // the LSU work interleaves with the fp64 work of the transform
+  auto store_quarter = [&](int item, int qtr) {
+    const int o = item / gcount, g = item % gcount;
+    double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+#pragma unroll
+    for (int it = 8 * qtr; it < 8 * qtr + 8; ++it) {
+      const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
+      yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
+    }
+  };
   if (it0 < it1) prefetch(it0);
   __syncthreads();
   // launched as a programmatic dependent of the transpose of n: everything above (twiddle table,
   // first operand prefetch) overlapped it; ng is read only after it completed
   pdl_entry();
+  tl_mark(a, 1, 1);
   if (a.skip && *a.skip) {
     cp_async_wait_all();
     return;
@@ -146,11 +180,35 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
-      if (!(a.dbg & 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
       // the previous item's tile goes out while step A runs (one instruction stream, so the
       // stores interleave with the transform); the first item stores its own (not yet written)
       // tile to its own destination, which its real store overwrites later in program order
-      if (!(a.dbg & 2)) store_tile(item == it0 ? item : item - 1);
+      const int sti = item == it0 ? item : item - 1;
+      if constexpr (SV == 0) {
+        if (!(a.dbg & 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
+        if (!(a.dbg & 2)) store_tile(sti);
+      } else {
+        // step A in pieces with a quarter of the tile store after each
+        double2 ea[16], ob[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          ea[r] = v[r];
+          ob[r] = mul_w32<-1>(v[r], r);
+        }
+        store_quarter(sti, 0);
+        Dft<16, -1>::run(ea);
+        store_quarter(sti, 1);
+        Dft<16, -1>::run(ob);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          v[2 * k] = ea[k];
+          v[2 * k + 1] = ob[k];
+        }
+        store_quarter(sti, 2);
+#pragma unroll
+        for (int k = 1; k < 32; ++k) v[k] = cmul(v[k], tw[k * 32 + lane]);
+        store_quarter(sti, 3);
+      }
       __syncthreads();  // every warp has read the tile: it is free for the exchanges
       if (!(a.dbg & 8)) warp_fft1024_tb<-1>(v, T, w, lane);
     }
@@ -195,6 +253,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     }
   }
   if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
+  tl_mark(a, 1, 2);
 }
 
 // Column pass, team variant: 16 warps per CTA, every 1024-point transform owned by a team of 64
@@ -532,7 +591,9 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   double2* twh = tw + 1024;        // W_2048^j, j < 1024
   __shared__ double2 tkk[8][32];
   // after the column pass completed: k_dvec (dependent) reads its moment partials
+  tl_mark(a, 2, 0);
   pdl_entry();
+  tl_mark(a, 2, 1);
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
             h = hw & 1, ht = tid & 127, bar = 1 + hf;
@@ -640,6 +701,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       bar_sync(bar, 128);  // the regions are reused by the next row pair
     }
   }
+  tl_mark(a, 2, 2);
 }
 
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
@@ -647,6 +709,8 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 // it runs on the SMs the last row launch leaves free, beside the row transforms.
 __global__ void __launch_bounds__(256, 2) k_dvec(RhsArgs a) {
   extern __shared__ double dsm[];  // 4 rf moment totals, 2 r gains, r + 2 scalars
+  tl_mark(a, 3, 0);
+  tl_mark(a, 3, 1);
   if (!(a.skip && *a.skip) && !(a.dbg & 256)) {
     const double* __restrict__ n = a.n.get();
     RhsArgs b = a;
@@ -723,9 +787,11 @@ __global__ void __launch_bounds__(256, 2) k_dvec(RhsArgs a) {
         a.dvec[s] = s == 0 ? epilogue0(b, n) : epilogue(b, n, s, 0.0);
     }
   }
+  tl_mark(a, 5, 2);  // D done (before the wait for the row grid)
   // launched as a programmatic dependent of the row kernel: do not complete before it does, so
   // the launches after this one see the row results (no-op for an ordinary launch)
   pdl_entry();
+  tl_mark(a, 3, 2);
 }
 
 // Inverse column pass: two real columns per complex 1024-pt inverse FFT, then S = birth + D.
@@ -738,10 +804,13 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   constexpr int GS = 2 * kCW + 1, GROWS = kW_N1 / 2 + 1;
   double2* tw = X + GROWS * GS;
   double* dv = reinterpret_cast<double*>(tw + 1024);  // [512][2 kCW] D values of the output tile
-  pdl_entry();
-  if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  // constant twiddle table: staged while the previous kernel drains (programmatic dependent launch)
+  tl_mark(a, 4, 0);
   for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
+  pdl_entry();
+  tl_mark(a, 4, 1);
+  if (a.skip && *a.skip) return;
   const double2* __restrict__ G = a.acc;
   const double scale = ldexp(0.5, -a.log2p);
   const bool birth = (a.flags & T_BIRTH) != 0;
@@ -750,18 +819,20 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   for (int grp = blockIdx.x; grp < kW_N2 / (2 * kCW); grp += gridDim.x) {
     const int col0 = grp * kCW * 2;
     __syncthreads();  // previous group's tile reads done
-    // G tile and the D values of this output tile, all in flight at once (cp.async)
+    // G tile and the D values of this output tile, all in flight at once (cp.async, two groups:
+    // the transforms wait for G only, the D values land while they run)
     for (int idx = tid; idx < GROWS * 2 * kCW; idx += kCW * 32) {
       const int row = idx / (2 * kCW), c = idx % (2 * kCW);
       cp_async16(X + row * GS + c, G + (int64_t)row * kW_N2 + col0 + c);
     }
+    cp_async_commit();
     for (int idx = tid; idx < kW_H * 2 * kCW; idx += kCW * 32) {
       const int nn1 = idx / (2 * kCW), c = idx % (2 * kCW);
       const int64_t jo = (int64_t)nn1 * kW_N2 + col0 + c + 1;
       cp_async8(dv + idx, a.dvec + (jo < a.m ? jo : 0), jo < a.m);
     }
     cp_async_commit();
-    cp_async_wait_all();
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
     __syncthreads();
     double2 v[32];
 #pragma unroll
@@ -778,7 +849,8 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
     }
     __syncthreads();  // tile consumed: the region becomes the exchange buffers
     warp_fft1024<+1, false>(v, X + w * kXR, tw, lane);
-    __syncthreads();  // all exchanges done: the regions become the birth tile
+    cp_async_wait_all();  // this thread's D values
+    __syncthreads();  // all exchanges done: the regions become the birth tile; every D value landed
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
       const int nn1 = lane + 32 * k;
@@ -794,6 +866,7 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
     if (grp == 0 && tid == 0) a.out[0] = a.dvec[0];
     __syncthreads();
   }
+  tl_mark(a, 4, 2);
 }
 
 static size_t smem_colm() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2) + 1024; }
@@ -816,7 +889,8 @@ cudaError_t rhs_w_set_smem_limits() {
   cudaError_t e;
 #define SET(fn, bytes) \
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
-  SET(k_colt, smem_colt());
+  SET(k_colt<0>, smem_colt());
+  SET(k_colt<1>, smem_colt());
   SET(k_colt2, smem_colt2());
   SET(k_colm, smem_colm());
   SET(k_rowd<false>, smem_rowd());
@@ -858,7 +932,12 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     } else if (getenv("AGK_COLT2") && atoi(getenv("AGK_COLT2")) == 1) {
       AGK_CK(launch_k(k_colt2, cgrid, 512, smem_colt2(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     } else {
-      AGK_CK(launch_k(k_colt, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
+      static const int stv = getenv("AGK_STV") ? atoi(getenv("AGK_STV")) : 1;  // 1: measured -3.5 us
+      if (stv == 1) {
+        AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
+      } else {
+        AGK_CK(launch_k(k_colt<0>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
+      }
     }
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
@@ -889,3 +968,15 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
 }
 
 }  // namespace agk
+
+// diagnostics only (tools/timeline.py): reset (reset != 0) or read the AGK_DBG & 512 timeline
+extern "C" int agk_dbg_timeline(unsigned long long* out, int reset) {
+  unsigned long long h[8][3];
+  if (reset) {
+    for (int k = 0; k < 8; ++k) h[k][0] = h[k][1] = ~0ull, h[k][2] = 0;
+    return (int)cudaMemcpyToSymbol(agk::g_timeline, h, sizeof(h));
+  }
+  const cudaError_t e = cudaMemcpyFromSymbol(h, agk::g_timeline, sizeof(h));
+  for (int k = 0; k < 24; ++k) out[k] = (&h[0][0])[k];
+  return (int)e;
+}

@@ -1,0 +1,27 @@
+"""Timeline of one config-4 RHS in graph mode (AGK_DBG=512 kernel stamps, %globaltimer):
+per kernel class the first CTA's arrival, the first CTA's start of work after its
+programmatic-dependency wait, and the last CTA's exit, in us from the first arrival."""
+import ctypes, os, sys
+os.environ["AGK_DBG"] = str(int(os.environ.get("AGK_DBG", "0")) | 512)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2407_16559_b200 as agk
+from paper_2407_16559_b200.configs import random_config4
+U, V, n = random_config4(1 << 20, 16)
+ws = agk.RhsWorkspace(agk.Model(U, V))
+nd = torch.from_numpy(n).cuda(); od = torch.empty_like(nd)
+lib = agk.load_library()
+buf = (ctypes.c_ulonglong * 24)()
+names = ["transpose", "col_fwd", "row", "dvec", "col_inv", "dvec(D done)"]
+agk.eval_rhs_timed(ws, nd, od, 5)
+for rep in range(3):
+    lib.agk_dbg_timeline(buf, 1)
+    ms = agk.eval_rhs_timed(ws, nd, od, 1)
+    lib.agk_dbg_timeline(buf, 0)
+    t = [[int(buf[3 * k + i]) for i in range(3)] for k in range(8)]
+    NONE = (0, 2**64 - 1)
+    t0 = min(t[k][0] for k in range(6) if t[k][0] not in NONE)
+    print(f"rep {rep}: graph {1e3 * ms:.1f} us")
+    for k in range(6):
+        f = lambda x: "    -  " if x in NONE else f"{(x - t0) / 1e3:7.1f}"
+        print(f"  {names[k]:14s} arrive {f(t[k][0])}  start {f(t[k][1])}  end {f(t[k][2])}")
