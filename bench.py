@@ -8,11 +8,12 @@ random positive low-rank kernel, R = 16, M = 2^20, fp64, seeded synthetic inputs
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 * value: K evaluations per rank on device-resident inputs, device time from CUDA events on the
-  handle's stream around the captured per-RHS graph (max over ranks); U/V (256 MiB) exceed the
+  handle's stream around captured graphs of 10 chained evaluations (max over ranks); U/V exceed the
   126 MB L2, so every evaluation streams them from HBM (no flush needed).
 * e2e: the same metric through the public C ABI (agk_rhs_eval) with pinned HOST buffers: the
   H2D copy of n and the D2H copy of S(n) are inside the timed region every step; `callers` host
-  threads (default 2), each with its own workspace, call concurrently (the reference's bench runs
+  threads (default 4: copies in both directions overlap the other callers' kernels), each with its
+  own workspace, call concurrently, at least 60 calls in all (the reference's bench runs
   cells on threads too), so copies overlap kernels; the one-caller figure is reported beside it.
 * roofline: the dominant kernel's algorithmic bytes per launch / its event-timed duration.
 * cpu_baseline: the reference compiled from its own sources (oracle/_ref), single thread, on a
@@ -50,7 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-callers", type=int, default=2)
+    ap.add_argument("--e2e-callers", type=int, default=4)
     ap.add_argument("--ref-budget-s", type=float, default=240.0)
     return ap.parse_args()
 
@@ -300,7 +301,7 @@ def run_b200(args, world, rank, local):
     calls(0, args.steps)
     single_sec = max_over_ranks(time.perf_counter() - t0, world, local)
     barrier(world)
-    per = max(1, args.steps // callers)
+    per = max(1, max(args.steps, 60) // callers)
     e2e_sec = max_over_ranks(timed_calls(per), world, local)
     for extra in wss[1:]:
         extra.close()

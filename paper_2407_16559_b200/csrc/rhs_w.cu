@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   // a quarter of the tile (8 lines per thread), fully unrolled: placed between pieces of step A so
   // the LSU work interleaves with the fp64 work of the transform
   auto store_quarter = [&](int item, int qtr) {
-    const int o = item / gcount, g = item % gcount;
+    int o = item / gcount, g = item % gcount;
+    if (a.dbg & 1024) o = blockIdx.x % 256, g = 0;  // experiment: one L2-resident tile per CTA
     double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
 #pragma unroll
     for (int it = 8 * qtr; it < 8 * qtr + 8; ++it) {
@@ -947,14 +948,19 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     }
     AGK_CK(launch_k(k_rowd<true>, rgrid, 256, smem_rowd(), s, pdl && (pdl_mask() & 4), a, g0, gc, (int)(g0 == 0)));
     if (mark) mark(mk, K_ROW, s);
-    // D on the SMs the row grid leaves free: k_dvec starts once every row CTA passed its wait
-    // (the column pass is complete) and waits for the row grid before it exits
+    // D (k_dvec) either beside the row pass, on the SMs its grid leaves free (it starts once every
+    // row CTA passed its wait, i.e. the column pass is complete, and waits for the row grid before
+    // it exits), or after it on every SM. Beside wins when the row pass outlasts D on the free SMs:
+    // measured at M = 2^20 (tools/timeline.py), row ~ 20 + 9.6 rf us and D on 19 SMs ~ 65 + 4 r us.
     const int free = nsm - rgrid;
-    // every k_dvec CTA must be resident from the start: a CTA that finished early would otherwise
-    // hold its SM slot in the final wait for the row grid, and the rest of D would run after it
-    static const int dv_per_sm = getenv("AGK_DVPS") ? atoi(getenv("AGK_DVPS")) : 2;
-    AGK_CK(launch_k(k_dvec, dv_per_sm * (free > 1 ? free : 1), 256, (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double), s,
-                    !mark, a));
+    const size_t dsm = (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double);
+    if (9.6 * a.rf >= 45.0 + 4.0 * a.r && free >= 8) {
+      // every k_dvec CTA must be resident from the start: a CTA that finished early would otherwise
+      // hold its SM slot in the final wait for the row grid, and the rest of D would run after it
+      AGK_CK(launch_k(k_dvec, 2 * free, 256, dsm, s, !mark, a));
+    } else {
+      AGK_CK(launch_k(k_dvec, 2 * nsm, 256, dsm, s, false, a));
+    }
     if (mark) mark(mk, K_DVEC, s);
   }
   static const bool civ4 = getenv("AGK_CIV") && atoi(getenv("AGK_CIV")) == 4;
