@@ -579,7 +579,7 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
         const cuuint64_t dims[2] = {(cuuint64_t)(2 * N2), (cuuint64_t)p.gsize * N1};
-        const cuuint64_t strides[1] = {(cuuint64_t)(2 * N2 * sizeof(double))};
+        const cuuint64_t strides[1] = {(cuuint64_t)(2 * (N2 + 8) * sizeof(double))};  // padded Y rows
         const cuuint32_t box[2] = {16, 256}, es[2] = {1, 1};
         const CUresult r = reinterpret_cast<Enc>(fn)(&h->plan.ytmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, y, dims, strides,
                                                      box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

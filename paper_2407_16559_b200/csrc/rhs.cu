@@ -446,7 +446,10 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->ytmap_ok = 0;
 }
 
-size_t rhs_y_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)p.gsize << p.log2p; }
+size_t rhs_y_elems(const RhsPlan& p) {
+  // rows padded by 8 entries (rhs_w.cu kW_YPAD; the other paths use the unpadded prefix)
+  return p.small ? 1 : (size_t)p.gsize * p.n1 * (p.n2 + 8);
+}
 size_t rhs_acc_elems(const RhsPlan& p) { return p.small ? 1 : (size_t)(p.n1 / 2 + 1) * p.n2; }
 size_t rhs_partial_elems(const RhsPlan& p, int rf) {
   const size_t nblk = p.small ? 1 : (size_t)p.n2;  // any column-block width >= 2, or one block per column

@@ -22,6 +22,10 @@
 namespace agk {
 
 constexpr int kW_N1 = 1024, kW_N2 = 2048, kW_H = kW_N1 / 2;
+// Y row stride (double2) and rank stride: rows padded by one 128-byte line, so the 1024 lines a
+// column item writes (one per row) do not all share the low address bits of a 32 KB stride
+constexpr int kW_YPAD = 8, kW_YS = kW_N2 + kW_YPAD;
+constexpr int64_t kW_YP = (int64_t)kW_N1 * kW_YS;
 // Region stride (double2) of the per-warp exchange / output regions: = 4 (mod 8) so that two
 // regions read at the same offset by neighbouring lanes sit on different 16-byte bank groups
 // (the tile store of k_colh and the split product of k_rowh both read region pairs that way).
@@ -112,23 +116,23 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   // the tile as full 128-byte row lines: slots (o & 1) * 1024 + 8 (o >> 1) + c of rank g's rows
   auto store_tile = [&](int item) {
     const int o = item / gcount, g = item % gcount;
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
 #pragma unroll 8
     for (int it = 0; it < kW_N1 / 32; ++it) {
       const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
-      yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
+      yg[(int64_t)row * kW_YS + c] = T[tile_idx(row, c)];
     }
   };
   // a quarter of the tile (8 lines per thread), fully unrolled: placed between pieces of step A so
   // the LSU work interleaves with the fp64 work of the transform
   auto store_quarter = [&](int item, int qtr) {
-    int o = item / gcount, g = item % gcount;
-    if (a.dbg & 1024) o = blockIdx.x % 256, g = 0;  // experiment: one L2-resident tile per CTA
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+    const int o = item / gcount, g = item % gcount;
+    if (a.dbg & 2) return;
+    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
 #pragma unroll
     for (int it = 8 * qtr; it < 8 * qtr + 8; ++it) {
       const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
-      yg[(int64_t)row * kW_N2 + c] = T[tile_idx(row, c)];
+      yg[(int64_t)row * kW_YS + c] = T[tile_idx(row, c)];
     }
   };
   if (it0 < it1) prefetch(it0);
@@ -206,8 +210,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
           v[2 * k + 1] = ob[k];
         }
         store_quarter(sti, 2);
-#pragma unroll
-        for (int k = 1; k < 32; ++k) v[k] = cmul(v[k], tw[k * 32 + lane]);
+        twiddle_a_rec<-1>(v, tw, lane);  // 5 shared loads instead of 31: the LSU is busy storing (-5 us)
         store_quarter(sti, 3);
       }
       __syncthreads();  // every warp has read the tile: it is free for the exchanges
@@ -297,11 +300,11 @@ __global__ void __launch_bounds__(512, 1) k_colt2(RhsArgs a, int g0, int gcount)
   // the tile as full 128-byte row lines (8 threads per row)
   auto store_tile = [&](int item) {
     const int o = item / gcount, g = item % gcount;
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_N1 * kW_N2 + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
+    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
 #pragma unroll 8
     for (int it = 0; it < kW_N1 * 8 / 512; ++it) {
       const int idx = tid + 512 * it, r = idx >> 3, p = idx & 7;
-      yg[(int64_t)r * kW_N2 + (p ^ ((r ^ (r >> 4) ^ (r >> 5)) & 7))] = T[idx];
+      yg[(int64_t)r * kW_YS + (p ^ ((r ^ (r >> 4) ^ (r >> 5)) & 7))] = T[idx];
     }
   };
   if (it0 < it1) prefetch(it0);
@@ -610,7 +613,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   double2* Xw = X + w * kXR;
   for (int k1 = 2 * blockIdx.x + hf; k1 < nrows; k1 += 2 * gridDim.x) {
     const int row = rho == 0 ? k1 : (n1 - k1) & (n1 - 1);
-    const double2* __restrict__ rsrc = a.y + (int64_t)row * kW_N2 + h * (kW_N2 / 2);
+    const double2* __restrict__ rsrc = a.y + (int64_t)row * kW_YS + h * (kW_N2 / 2);
     double2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j];
@@ -645,7 +648,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
         }
         if (k1n < nrows) {
           const int rown = rho == 0 ? k1n : (n1 - k1n) & (n1 - 1);
-          prefetch_l2(a.y + (int64_t)gn * P + (int64_t)rown * kW_N2 + h * (kW_N2 / 2), 1024 * sizeof(double2));
+          prefetch_l2(a.y + (int64_t)gn * kW_YP + (int64_t)rown * kW_YS + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
       if (!(a.dbg & 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
       if (g + 1 < gcount && !(a.dbg & 64)) {
-        const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * P;
+        const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * kW_YP;
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       }
