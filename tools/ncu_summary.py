@@ -78,7 +78,7 @@ def launches(path):
             continue
         v = _num(r[hdr.index("Metric Value")])
         unit = r[hdr.index("Metric Unit")]
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         a = agg.setdefault(r[hdr.index("Kernel Name")], [0, 0.0])
         a[0] += 1
         a[1] += v
