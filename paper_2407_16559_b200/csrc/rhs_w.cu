@@ -610,7 +610,6 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   }
   __syncthreads();
   double2* Xh = X + hf * 4 * kXR;
-  if (hf == 1 && (a.dbg >> 16)) __nanosleep(((a.dbg >> 16) & 255) * 32);  // experiment: offset the halves
   double2* Xw = X + w * kXR;
   for (int k1 = 2 * blockIdx.x + hf; k1 < nrows; k1 += 2 * gridDim.x) {
     const int row = rho == 0 ? k1 : (n1 - k1) & (n1 - 1);

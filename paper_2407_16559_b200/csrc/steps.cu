@@ -71,13 +71,22 @@ struct CombArgs {
 
 __device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
 
+// stage-vector inputs of each combination and the y slot each comes from
+__host__ __device__ constexpr int comb_inputs(int kind) {
+  return kind == C_RK2_ST || kind == C_RK4_STH || kind == C_RK4_ST1 || kind == C_F2 ? 1
+         : kind == C_RK2_OUT || kind == C_F3                                      ? 2
+         : kind == C_F4                                                           ? 3
+         : kind == C_RK4_OUT || kind == C_F5                                      ? 4
+                                                                                  : 5;  // C_F6, C_F_OUT
+}
+__host__ __device__ constexpr int comb_slot(int kind, int j) { return kind == C_F_OUT && j > 0 ? j + 1 : j; }
+
 template <int KIND, bool RED>
 __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
   pdl_entry();
   const double t = a.tau_mul * a.ctl->tau;
   const double* __restrict__ x = a.x.get();
   double* __restrict__ out = a.out.get();
-  const double *y0 = a.y[0], *y1 = a.y[1], *y2 = a.y[2], *y3 = a.y[3], *y4 = a.y[4], *y5 = a.y[5];
   const bool store5 = (KIND == C_F_OUT) && a.ctl->store_n5;
   double acc[RF_N];
   if (RED) {
@@ -85,46 +94,67 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
     for (int q = 0; q < RF_N; ++q) acc[q] = 0.0;
     acc[RF_MIN] = __longlong_as_double(0x7ff0000000000000LL);
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
-    const double xi = x[i];
-    double o, other = 0.0;
-    using namespace rkf;
-    switch (KIND) {
-      case C_RK2_ST: o = xi + t * y0[i]; break;
-      case C_RK2_OUT: o = xi + 0.5 * t * (y0[i] + y1[i]); break;
-      case C_RK4_STH: o = xi + 0.5 * t * y0[i]; break;
-      case C_RK4_ST1: o = xi + t * y0[i]; break;
-      case C_RK4_OUT: o = xi + t * (y0[i] + 2.0 * y1[i] + 2.0 * y2[i] + y3[i]) / 6.0; break;
-      case C_F2: o = xi + t * a21 * y0[i]; break;
-      case C_F3: o = xi + t * (a31 * y0[i] + a32 * y1[i]); break;
-      case C_F4: o = xi + t * (a41 * y0[i] + a42 * y1[i] + a43 * y2[i]); break;
-      case C_F5: o = xi + t * (a51 * y0[i] + a52 * y1[i] + a53 * y2[i] + a54 * y3[i]); break;
-      case C_F6: o = xi + t * (a61 * y0[i] + a62 * y1[i] + a63 * y2[i] + a64 * y3[i] + a65 * y4[i]); break;
-      default: {  // C_F_OUT
-        const double k1 = y0[i], k3 = y2[i], k4 = y3[i], k5 = y4[i], k6 = y5[i];
-        other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
-        o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
-        if (store5) a.n5[i] = other;
-        break;
-      }
+  // kU elements per thread per step, all their loads issued before any arithmetic: a pass over
+  // 8 MiB vectors needs that memory-level parallelism from 2 CTAs per SM (the partial-sum CTAs)
+  constexpr int kU = 4;
+  constexpr int NY = comb_inputs(KIND);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < a.m; i0 += kU * stride) {
+    double xv[kU], yv[NY > 0 ? NY : 1][kU], ov[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int64_t i = i0 + q * stride < a.m ? i0 + q * stride : i0;  // clamped: unpredicated loads
+      xv[q] = x[i];
+#pragma unroll
+      for (int j = 0; j < NY; ++j) yv[j][q] = a.y[comb_slot(KIND, j)][i];
+      ov[q] = (RED && KIND != C_F_OUT && a.other) ? a.other[i] : 0.0;
     }
-    out[i] = o;
-    if (RED) {
-      if (KIND != C_F_OUT && a.other) other = a.other[i];
-      if (KIND == C_F_OUT || a.other) {
-        const double d = o - other;
-        acc[RF_ERR2] += d * d;
-        if (!finite_d(other)) acc[RF_NF_OTHER] = 1.0;
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int64_t i = i0 + q * stride;
+      if (i >= a.m) break;
+      const double xi = xv[q];
+      double o, other = 0.0;
+      using namespace rkf;
+      switch (KIND) {
+        case C_RK2_ST: o = xi + t * yv[0][q]; break;
+        case C_RK2_OUT: o = xi + 0.5 * t * (yv[0][q] + yv[1][q]); break;
+        case C_RK4_STH: o = xi + 0.5 * t * yv[0][q]; break;
+        case C_RK4_ST1: o = xi + t * yv[0][q]; break;
+        case C_RK4_OUT: o = xi + t * (yv[0][q] + 2.0 * yv[1][q] + 2.0 * yv[2][q] + yv[3][q]) / 6.0; break;
+        case C_F2: o = xi + t * a21 * yv[0][q]; break;
+        case C_F3: o = xi + t * (a31 * yv[0][q] + a32 * yv[1][q]); break;
+        case C_F4: o = xi + t * (a41 * yv[0][q] + a42 * yv[1][q] + a43 * yv[2][q]); break;
+        case C_F5: o = xi + t * (a51 * yv[0][q] + a52 * yv[1][q] + a53 * yv[2][q] + a54 * yv[3][q]); break;
+        case C_F6:
+          o = xi + t * (a61 * yv[0][q] + a62 * yv[1][q] + a63 * yv[2][q] + a64 * yv[3][q] + a65 * yv[4][q]);
+          break;
+        default: {  // C_F_OUT: inputs k1, k3, k4, k5, k6
+          const double k1 = yv[0][q], k3 = yv[1][q], k4 = yv[2][q], k5 = yv[3][q], k6 = yv[4][q];
+          other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
+          o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
+          if (store5) a.n5[i] = other;
+          break;
+        }
       }
-      if (!finite_d(o)) acc[RF_NF_CAND] = 1.0;
-      const double kk = (double)(i + 1);
-      acc[RF_L2SQ] += o * o;
-      acc[RF_MOM0] += o;
-      acc[RF_MOM1] += kk * o;
-      acc[RF_MOM2] += kk * kk * o;
-      acc[RF_MIN] = o < acc[RF_MIN] ? o : acc[RF_MIN];
-      const double ab = fabs(o);
-      acc[RF_MAXABS] = acc[RF_MAXABS] < ab ? ab : acc[RF_MAXABS];
+      out[i] = o;
+      if (RED) {
+        if (KIND != C_F_OUT && a.other) other = ov[q];
+        if (KIND == C_F_OUT || a.other) {
+          const double d = o - other;
+          acc[RF_ERR2] += d * d;
+          if (!finite_d(other)) acc[RF_NF_OTHER] = 1.0;
+        }
+        if (!finite_d(o)) acc[RF_NF_CAND] = 1.0;
+        const double kk = (double)(i + 1);
+        acc[RF_L2SQ] += o * o;
+        acc[RF_MOM0] += o;
+        acc[RF_MOM1] += kk * o;
+        acc[RF_MOM2] += kk * kk * o;
+        acc[RF_MIN] = o < acc[RF_MIN] ? o : acc[RF_MIN];
+        const double ab = fabs(o);
+        acc[RF_MAXABS] = acc[RF_MAXABS] < ab ? ab : acc[RF_MAXABS];
+      }
     }
   }
   if (RED) {
