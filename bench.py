@@ -18,6 +18,8 @@ random positive low-rank kernel, R = 16, M = 2^20, fp64, seeded synthetic inputs
 * roofline: the dominant kernel's algorithmic bytes per launch / its event-timed duration.
 * cpu_baseline: the reference compiled from its own sources (oracle/_ref), single thread, on a
   bounded sample (2 evaluations) on rank 0.
+* adaptive: the metric's time-to-t_end half, live: config 5 (M = 2^20, Brownian + source) RKF45
+  on the device to t = 200 (a prefix of t_end = 1e5; full horizons in profiles/runs_*.json).
 * --impl reference: the reference's CPU implementation on all host cores (one independent
   evaluation per thread, as the reference's own bench runs cells on std::threads).
 * N > 1: replicas only (the path does not shard): one independent workload per GPU,
@@ -53,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-callers", type=int, default=4)
     ap.add_argument("--ref-budget-s", type=float, default=240.0)
+    ap.add_argument("--adaptive-horizon", type=float, default=200.0,
+                    help="config-5 RKF45 adaptive solve to this t (0: skip); t_end is 1e5")
     return ap.parse_args()
 
 
@@ -369,10 +373,38 @@ def run_b200(args, world, rank, local):
         "e2e": e2e, "roofline": roofline, "gpu_launches": launches * args.steps,
         "clocks": clk.summary(),
     }
+    ws.close()
+    if args.adaptive_horizon > 0:
+        res["adaptive"] = adaptive_leg(args, world, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_sample(U, V, n)
-    ws.close()
     return res
+
+
+def adaptive_leg(args, world, local):
+    """The metric's second half, measured live: a device-resident adaptive solve of BASELINE
+    config 5 (Brownian kernel + monomer source, M = 2^20, R = 3, n0 = 0, RKF45, tol 1e-6) to
+    t = --adaptive-horizon, a prefix of its t_end = 1e5 (the full horizons are tools/runs.py runs,
+    profiles/runs_*.json). Wall time around agk.run (graph build excluded: built by a first short
+    run), accepted steps/s and the in-run time per RHS evaluation."""
+    import torch
+    import paper_2407_16559_b200 as agk
+    from paper_2407_16559_b200.configs import baseline_config
+    cfg = baseline_config(5)
+    ws = agk.RhsWorkspace(agk.Model(cfg["u"], cfg["v"], cfg["variant"], cfg["sources"], cfg["lam"]), device=local)
+    ctl = agk.StepControl(stepper=agk.RKF45, tol=cfg["tol"])
+    agk.run(ws, agk.SimulationConfig(ctl, 1.0, cfg["n0"]))  # builds and instantiates the step graph
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rep = agk.run(ws, agk.SimulationConfig(ctl, args.adaptive_horizon, cfg["n0"]))
+    wall = max_over_ranks(time.perf_counter() - t0, world, local)
+    ws.close()
+    return {"workload": f"config5 RKF45 tol 1e-6, M=2^20 R=3, t in [0, {args.adaptive_horizon:g}] (t_end 1e5)",
+            "termination": rep.termination, "final_t": rep.final_t, "wall_s": wall,
+            "accepted": rep.total_accepted, "rejects": rep.total_rejects, "rhs_evals": rep.total_rhs_evals,
+            "accepted_steps_per_s": world * rep.total_accepted / wall,
+            "us_per_rhs_in_run": 1e6 * wall / max(rep.total_rhs_evals, 1)}
 
 
 def main():

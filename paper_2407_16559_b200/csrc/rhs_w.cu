@@ -625,16 +625,20 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     // the radix-2 twiddles of this thread's bins, the same for every rank: W_2048^q' for q' = ht +
     // 128 j (row k1) and, with the combination's sign folded in, -W_2048^-m' for the partner bins
     // of row N1-k1 (m' = 1023 - q', or N2 - q for row 0, whose bin 0 pairs with itself unrotated)
+    // (hoisted into registers for the last launch; the accumulating launches of a multi-group
+    // plan, which also carry the accumulator through global memory, form them per rank instead,
+    // where the 32 extra live registers would spill)
     double2 tw1[8], tw2[8];
-    {
-      const double2 wb1 = twh[ht];
-      // W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1)), negated
-      const double2 wb2 = k1 == 0 ? make_double2(wb1.x, -wb1.y) : make_double2(twh[ht + 1].x, -twh[ht + 1].y);
+    const double2 wb1 = twh[ht];
+    // W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1)), negated
+    const double2 wb2 = k1 == 0 ? make_double2(wb1.x, -wb1.y) : make_double2(twh[ht + 1].x, -twh[ht + 1].y);
+    auto tw_of = [&](int j, double2& t1w, double2& t2w) {
+      t1w = mul_w16<-1>(wb1, j);
+      t2w = (k1 == 0 && ht == 0 && j == 0) ? make_double2(1.0, 0.0) : mul_w16<+1>(wb2, j);
+    };
+    if constexpr (LAST) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        tw1[j] = mul_w16<-1>(wb1, j);
-        tw2[j] = (k1 == 0 && ht == 0 && j == 0) ? make_double2(1.0, 0.0) : mul_w16<+1>(wb2, j);
-      }
+      for (int j = 0; j < 8; ++j) tw_of(j, tw1[j], tw2[j]);
     }
     for (int g = 0; g < gcount; ++g) {
       const double wq = 0.25 * a.uniq_weight[g0 + g];
@@ -651,7 +655,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           prefetch_l2(a.y + (int64_t)gn * kW_YP + (int64_t)rown * kW_YS + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
-      if (!(a.dbg & 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence
+      if (!(a.dbg & 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
@@ -669,7 +673,14 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
         const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
         const double2 e1 = Xh[qp], o1 = Xh[kXR + qp];
         const double2 e2 = Xh[2 * kXR + m], o2 = Xh[3 * kXR + m];
-        const double2 t1 = cmul(o1, tw1[j]), t2 = cmul(o2, tw2[j]);
+        double2 t1w, t2w;
+        if constexpr (LAST) {
+          t1w = tw1[j];
+          t2w = tw2[j];
+        } else {
+          tw_of(j, t1w, t2w);
+        }
+        const double2 t1 = cmul(o1, t1w), t2 = cmul(o2, t2w);
         const double2 xa = cadd(e1, t1), xb = csub(e1, t1);
         const double2 pa = cadd(e2, t2), pb = csub(e2, t2);
         split_product_acc4(acc[j], wq, xa, pa);
