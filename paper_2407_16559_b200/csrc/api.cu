@@ -569,24 +569,6 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
       CK_C(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, hp->device), "SM count");
       h->plan.nsm = nsm;
     }
-    {
-      // TMA descriptor for the column pass' tile stores into Y
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess && fn &&
-          q == cudaDriverEntryPointSuccess) {
-        using Enc = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-        const cuuint64_t dims[2] = {(cuuint64_t)(2 * N2), (cuuint64_t)p.gsize * N1};
-        const cuuint64_t strides[1] = {(cuuint64_t)(2 * (N2 + 8) * sizeof(double))};  // padded Y rows
-        const cuuint32_t box[2] = {16, 256}, es[2] = {1, 1};
-        const CUresult r = reinterpret_cast<Enc>(fn)(&h->plan.ytmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, y, dims, strides,
-                                                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        h->plan.ytmap_ok = r == CUDA_SUCCESS;
-      }
-    }
     a.uvg = uvg;
     a.ng = ng;
     a.tw32 = dt32;

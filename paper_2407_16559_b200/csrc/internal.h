@@ -89,10 +89,6 @@ struct RhsPlan {
   int launches;  // kernels per RHS
   // SM count (grid sizing of the fast path)
   int nsm;
-  // fast path: TMA descriptor of Y viewed as [gsize * N1 rows][2 * N2 doubles], 128-byte
-  // swizzle, box 16 doubles x 256 rows (column-tile stores); valid when ytmap_ok
-  CUtensorMap ytmap;
-  int ytmap_ok;
 };
 
 // kernel classes for per-launch timing

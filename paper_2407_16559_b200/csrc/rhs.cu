@@ -443,7 +443,6 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);  // fast: + transpose, dvec
   p->nsm = 148;
   p->dense = 0;
-  p->ytmap_ok = 0;
 }
 
 size_t rhs_y_elems(const RhsPlan& p) {

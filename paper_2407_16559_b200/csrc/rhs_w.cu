@@ -260,322 +260,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   tl_mark(a, 1, 2);
 }
 
-// Column pass, team variant: 16 warps per CTA, every 1024-point transform owned by a team of 64
-// threads with 16 points each (16 x 16 x 4: registers, exchange, registers, exchange, radix 4),
-// ~128 registers per thread, so twice the warps of k_colt hide the memory and shared-memory
-// latencies. Same items (column octet, rank), tile, Y layout and moment partials as k_colt.
-// Team q owns chunk q ^ g(r) of tile row r, g(r) = (r ^ (r >> 4) ^ (r >> 5)) & 7; exchange 1 puts
-// entry (k1, t) at row 64 k1 + t, exchange 2 entry (k1, s, a) at row 64 k1 + 4 a + s, the output
-// K at row K — every access pattern is conflict-free (exhaustive search, tools/probe).
-__device__ __forceinline__ int t2_idx(int r, int q) { return r * 8 + (q ^ ((r ^ (r >> 4) ^ (r >> 5)) & 7)); }
-__device__ __forceinline__ void team_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-__global__ void __launch_bounds__(512, 1) k_colt2(RhsArgs a, int g0, int gcount) {
-  extern __shared__ double2 smem[];
-  double2* T = smem;               // 1024 x 8 tile: exchanges + output (t2_idx)
-  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
-  double2* tw1 = S + 8 * kW_H;     // W_1024^{t k1}, [k1][t] (16 x 64)
-  double2* tw2 = tw1 + 1024;       // W_64^e, e < 64
-  __shared__ double red[16][4];
-  __shared__ double2 tkf[8][8];    // per team: W_P^{16 n2 i}, W_P^{256 n2 b} (i, b < 4)
-  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, team = tid >> 6, t = tid & 63;
-  const int k1t = t >> 2, st = t & 3;  // this thread's (k1, s) after the first exchange
-  const int bar = 1 + team;
-  const int items = (kW_N2 / 8) * gcount;
-  const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
-  const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
-  for (int i = tid; i < 1024; i += blockDim.x) tw1[i] = tw_p<-1>(a.twp, (uint32_t)(2048 * (i & 63) * (i >> 6)));
-  for (int i = tid; i < 64; i += blockDim.x) tw2[i] = tw_p<-1>(a.twp, (uint32_t)(32768 * i));
-  double2* St = S + team * kW_H;
-  auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * team + (o & 1); };
-  auto src_of = [&](int item) {
-    const int o = item / gcount, ub = g0 + item % gcount;
-    return a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
-  };
-  auto prefetch = [&](int item) {
-    const double2* src = src_of(item);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) cp_async16(St + t + 64 * q, src + t + 64 * q);
-    cp_async_commit();
-  };
-  // the tile as full 128-byte row lines (8 threads per row)
-  auto store_tile = [&](int item) {
-    const int o = item / gcount, g = item % gcount;
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
-#pragma unroll 8
-    for (int it = 0; it < kW_N1 * 8 / 512; ++it) {
-      const int idx = tid + 512 * it, r = idx >> 3, p = idx & 7;
-      yg[(int64_t)r * kW_YS + (p ^ ((r ^ (r >> 4) ^ (r >> 5)) & 7))] = T[idx];
-    }
-  };
-  if (it0 < it1) prefetch(it0);
-  __syncthreads();
-  pdl_entry();
-  if (a.skip && *a.skip) {
-    cp_async_wait_all();
-    return;
-  }
-  double nl[8];
-  double2 base = czero();
-  int cur_o = -1;
-  for (int item = it0; item < it1; ++item) {
-    const int o = item / gcount, g = item % gcount, ub = g0 + g;
-    const int n2 = col_of(o);
-    if (o != cur_o) {
-      cur_o = o;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + t + 64 * r];
-      base = tw_p<-1>(a.twp, (uint32_t)(n2 * (k1t + 64 * st)));
-      if (t < 8) tkf[team][t] = tw_p<-1>(a.twp, (uint32_t)(n2 * (t < 4 ? 16 * t : 256 * (t - 4))));
-    }
-    cp_async_wait_all();
-    team_bar(bar);  // the team's staged operands (and tkf) are visible
-    double2 v[16];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-      const double2 uv = St[t + 64 * r];
-      const double x = uv.x * nl[r], y = uv.y * nl[r];
-      v[r] = make_double2(x, y);
-      const int64_t i = (int64_t)(t + 64 * r) * kW_N2 + n2;  // zero-filled past m
-      if (i >= 1) {
-        const double sz = (double)(i + 1);
-        s0 += x;
-        s1 += sz * x;
-        s2 += y;
-        s3 += sz * y;
-      }
-    }
-#pragma unroll
-    for (int r = 8; r < 16; ++r) v[r] = czero();
-    team_bar(bar);  // staging region consumed by the whole team
-    if (item + 1 < it1) prefetch(item + 1);
-    if (item + a.pfd + 1 < it1 && t == 0) prefetch_l2(src_of(item + a.pfd + 1), kW_H * sizeof(double2));
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    if (lane == 0) {
-      red[wp][0] = s0;
-      red[wp][1] = s1;
-      red[wp][2] = s2;
-      red[wp][3] = s3;
-    }
-    // step A: DFT_16 over r (upper half zero), twiddle W_1024^{t k1}
-    dft_halfzero<16, -1>(v);
-#pragma unroll
-    for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw1[k1 * 64 + t]);
-    if (!(a.dbg & 2)) store_tile(item == it0 ? item : item - 1);
-    __syncthreads();  // tile free for the exchanges
-#pragma unroll
-    for (int k1 = 0; k1 < 16; ++k1) T[t2_idx(64 * k1 + t, team)] = v[k1];
-    team_bar(bar);
-#pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = T[t2_idx(64 * k1t + st + 4 * u, team)];
-    Dft<16, -1>::run(v);  // over u -> a
-#pragma unroll
-    for (int aa = 1; aa < 16; ++aa) v[aa] = cmul(v[aa], tw2[st * aa]);
-    team_bar(bar);
-#pragma unroll
-    for (int aa = 0; aa < 16; ++aa) T[t2_idx(64 * k1t + 4 * aa + st, team)] = v[aa];
-    team_bar(bar);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      double2 q[4];
-      const int aa = 4 * st + i;
-#pragma unroll
-      for (int ss = 0; ss < 4; ++ss) q[ss] = T[t2_idx(64 * k1t + 4 * aa + ss, team)];
-      Dft<4, -1>::run(q);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) v[4 * i + b] = q[b];
-    }
-    team_bar(bar);
-    // output K = k1 + 16 (4 s + i) + 256 b with the four-step twiddle W_P^{n2 K}
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double2 ci = cmul(base, tkf[team][i]);
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int K = k1t + 16 * (4 * st + i) + 256 * b;
-        T[t2_idx(K, team)] = cmul(v[4 * i + b], cmul(ci, tkf[team][4 + b]));
-      }
-    }
-    __syncthreads();  // the output tile and every warp's sums are complete
-    if (tid < 4) {
-      double tt = 0.0;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) tt += red[q][tid];
-      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = tt;
-    }
-  }
-  if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
-}
 
-// Column pass with TMA tile stores and no CTA-wide barrier in the loop (warps drift apart, so
-// one warp's memory phase overlaps another's transform). As k_colt, an item is (column octet,
-// rank) and the 8 warps' outputs form a 1024 x 8 tile of 16-byte chunks written back as full
-// 128-byte Y row lines — here by four bulk tensor stores (TMA, 128-byte swizzle) issued by the
-// last warp to finish its output, so the copy-out runs on the TMA engine.
-// Every access to the tile uses the TMA swizzle: warp w owns chunk w ^ (r & 7) of physical row
-// r. Output entry i sits at row i; the exchange runs through rows r(i) = i ^ ((i >> 5) & 7), which
-// keeps both exchange patterns (i = 32k + lane, i = 32 lane + l) conflict-free. Since a warp only
-// ever touches its own chunk of each row, the exchange and the output need no barrier between
-// warps; the only cross-warp dependencies are "all 8 outputs written" (shared counter, the 8th
-// warp issues the stores) and "the previous tile has been read by the TMA" (mbarrier the issuing
-// thread arrives on once its bulk group's reads completed), waited for before each exchange.
-// Moment sums are written per warp (8 partial blocks per octet).
-__device__ __forceinline__ int xch_idx(int i, int w) {
-  const int r = i ^ ((i >> 5) & 7);
-  return r * 8 + (w ^ (r & 7));
-}
-__device__ __forceinline__ int out_idx(int i, int w) { return i * 8 + (w ^ (i & 7)); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n}" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-          (unsigned)__cvta_generic_to_shared(b)),
-      "r"(parity) : "memory");
-}
-__global__ void __launch_bounds__(256, 1) k_colm(RhsArgs a, int g0, int gcount, const __grid_constant__ CUtensorMap ytm) {
-  extern __shared__ double2 smem_raw[];
-  double2* T = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
-  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
-  __shared__ double2 tk[8][32];
-  __shared__ uint64_t empty_bar;   // phase j completes when the bulk stores of local item j read T
-  __shared__ unsigned done_cnt;    // warps that finished their output, over all items
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int items = (kW_N2 / 8) * gcount;
-  const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
-  const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
-  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
-  if (tid == 0) {
-    mbar_init(&empty_bar, 1);
-    done_cnt = 0;
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  double2* Sw = S + w * kW_H;
-  auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * w + (o & 1); };
-  auto src_of = [&](int item) {
-    const int o = item / gcount, ub = g0 + item % gcount;
-    return a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
-  };
-  auto prefetch = [&](int item) {
-    const double2* src = src_of(item);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
-    cp_async_commit();
-  };
-  const uint32_t tsm = (uint32_t)__cvta_generic_to_shared(T);
-  const uint64_t tmp = reinterpret_cast<uint64_t>(&ytm);
-  if (it0 < it1) prefetch(it0);
-  __syncthreads();
-  pdl_entry();
-  if (a.skip && *a.skip) {
-    cp_async_wait_all();
-    return;
-  }
-  bool issuer = false;  // this thread issued the bulk stores of the previous item
-  double nl[16];
-  double2 base = czero();
-  int cur_o = -1;
-  for (int item = it0; item < it1; ++item) {
-    const int j = item - it0;
-    const int o = item / gcount, g = item % gcount, ub = g0 + g;
-    const int n2 = col_of(o);
-    if (o != cur_o) {
-      cur_o = o;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
-      base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
-      __syncwarp();
-      tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    double2 v[32];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const double2 uv = Sw[lane + 32 * r];
-      const double x = uv.x * nl[r], y = uv.y * nl[r];
-      v[r] = make_double2(x, y);
-      const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
-      if (i >= 1) {
-        const double sz = (double)(i + 1);
-        s0 += x;
-        s1 += sz * x;
-        s2 += y;
-        s3 += sz * y;
-      }
-    }
-#pragma unroll
-    for (int r = 16; r < 32; ++r) v[r] = czero();
-    __syncwarp();
-    if (item + 1 < it1) prefetch(item + 1);
-    if (item + a.pfd + 1 < it1 && lane == 0) prefetch_l2(src_of(item + a.pfd + 1), kW_H * sizeof(double2));
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    if (lane < 4) {
-      const double t = lane == 0 ? s0 : lane == 1 ? s1 : lane == 2 ? s2 : s3;
-      a.partials[((int64_t)ub * (kW_N2 / 8) * 8 + o * 8 + w) * 4 + lane] = t;
-    }
-    warp_fft1024_a<-1, true>(v, tw, lane);
-    if (j > 0) {
-      // the previous tile must have been read by its bulk stores before the exchange reuses it
-      if (issuer) {
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(&empty_bar);
-        issuer = false;
-      }
-      mbar_wait(&empty_bar, (unsigned)((j - 1) & 1));
-    }
-#pragma unroll
-    for (int k = 0; k < 32; ++k) T[xch_idx(32 * k + lane, w)] = v[k];
-    __syncwarp();
-#pragma unroll
-    for (int l = 0; l < 32; ++l) v[l] = T[xch_idx(32 * lane + l, w)];
-    Dft<32, -1>::run(v);
-    __syncwarp();
-    // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
-#pragma unroll
-    for (int k = 0; k < 32; ++k) T[out_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
-    // make this warp's writes visible to the TMA (async proxy), then count the warp in
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    unsigned prev = 0;
-    if (lane == 0) {
-      asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
-                   : "=r"(prev) : "r"((unsigned)__cvta_generic_to_shared(&done_cnt)) : "memory");
-    }
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if ((prev & 7) == 7 && lane == 0 && !(a.dbg & 2)) {
-      // the 8th warp: every output of this item is in T
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      const int x = 2 * ((o & 1) * (kW_N2 / 2) + 8 * (o >> 1));
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int yrow = g * kW_N1 + 256 * b;
-        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                     ::"l"(tmp), "r"(x), "r"(yrow), "r"(tsm + b * 256 * 128) : "memory");
-      }
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      issuer = true;
-    } else if ((prev & 7) == 7 && lane == 0) {
-      issuer = true;  // (stores disabled for experiments) still release the tile
-    }
-  }
-  if (issuer) {
-    if (!(a.dbg & 2)) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  }
-}
 
 // Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
 // row pair (k1, N1-k1) at a time with warps (rho, h) = (row, even/odd samples). Per rank a warp
@@ -884,8 +569,6 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   tl_mark(a, 4, 2);
 }
 
-static size_t smem_colm() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2) + 1024; }
-static size_t smem_colt2() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024 + 64) * sizeof(double2); }
 static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
 template <int CW>
@@ -906,8 +589,6 @@ cudaError_t rhs_w_set_smem_limits() {
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
   SET(k_colt<0>, smem_colt());
   SET(k_colt<1>, smem_colt());
-  SET(k_colt2, smem_colt2());
-  SET(k_colm, smem_colm());
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
   SET(k_colinvw<8>, smem_colinvw());
@@ -940,19 +621,11 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
     const int cgrid = items < nsm ? items : nsm;
-    static const bool tma = getenv("AGK_COLTMA") && atoi(getenv("AGK_COLTMA")) == 1;  // opt-in: measured slower
-    if (tma && p.ytmap_ok) {
-      a.nblk_colfwd = kW_N2;  // per-warp moment partials
-      AGK_CK(launch_k(k_colm, cgrid, 256, smem_colm(), s, pdl, a, g0, gc, p.ytmap));
-    } else if (getenv("AGK_COLT2") && atoi(getenv("AGK_COLT2")) == 1) {
-      AGK_CK(launch_k(k_colt2, cgrid, 512, smem_colt2(), s, pdl && (pdl_mask() & 2), a, g0, gc));
+    static const int stv = getenv("AGK_STV") ? atoi(getenv("AGK_STV")) : 1;  // 1: measured -3.5 us
+    if (stv == 1) {
+      AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     } else {
-      static const int stv = getenv("AGK_STV") ? atoi(getenv("AGK_STV")) : 1;  // 1: measured -3.5 us
-      if (stv == 1) {
-        AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
-      } else {
-        AGK_CK(launch_k(k_colt<0>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
-      }
+      AGK_CK(launch_k(k_colt<0>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     }
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
