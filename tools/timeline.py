@@ -1,4 +1,4 @@
-"""Timeline of one config-4 RHS in graph mode (AGK_DBG=512 kernel stamps, %globaltimer):
+"""Timeline of one config-4 (or config-5: argv[1]) RHS in graph mode (AGK_DBG=512 kernel stamps, %globaltimer):
 per kernel class the first CTA's arrival, the first CTA's start of work after its
 programmatic-dependency wait, and the last CTA's exit, in us from the first arrival."""
 import ctypes, os, sys
@@ -6,10 +6,12 @@ os.environ["AGK_DBG"] = str(int(os.environ.get("AGK_DBG", "0")) | 512)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2407_16559_b200 as agk
-from paper_2407_16559_b200.configs import random_config4
-U, V, n = random_config4(1 << 20, 16)
-ws = agk.RhsWorkspace(agk.Model(U, V))
-nd = torch.from_numpy(n).cuda(); od = torch.empty_like(nd)
+from paper_2407_16559_b200.configs import baseline_config
+cfg = baseline_config(int(sys.argv[1]) if len(sys.argv) > 1 else 4)  # a P = 2^21 config: 4 or 5
+m = cfg["u"].shape[0]
+ws = agk.RhsWorkspace(agk.Model(cfg["u"], cfg["v"], cfg["variant"], cfg["sources"], cfg["lam"]))
+n = cfg["n0"] if cfg.get("tol") is None else np.random.default_rng(0).random(m) * np.exp(-np.arange(m) / (m / 8))
+nd = torch.from_numpy(np.ascontiguousarray(n)).cuda(); od = torch.empty_like(nd)
 lib = agk.load_library()
 buf = (ctypes.c_ulonglong * 24)()
 names = ["transpose", "col_fwd", "row", "dvec", "col_inv", "dvec(D done)"]
