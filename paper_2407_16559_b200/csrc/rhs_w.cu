@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     for (int r = 16; r < 32; ++r) v[r] = czero();
     __syncwarp();
     if (item + 1 < it1) prefetch(item + 1);
-    if (item + a.pfd + 1 < it1 && lane == 0 && !(a.dbg & 128)) {
+    // L2 bulk prefetch of the item after next: opt-in (AGK_DBG & 32768) since the tile store is
+    // interleaved with step A (measured 1.5-2 us faster without; the row pass keeps its prefetch)
+    if (item + a.pfd + 1 < it1 && lane == 0 && (a.dbg & 32768)) {
       const int o2 = (item + a.pfd + 1) / gcount, ub2 = g0 + (item + a.pfd + 1) % gcount;
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
