@@ -94,66 +94,101 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
     for (int q = 0; q < RF_N; ++q) acc[q] = 0.0;
     acc[RF_MIN] = __longlong_as_double(0x7ff0000000000000LL);
   }
-  // kU elements per thread per step, all their loads issued before any arithmetic: a pass over
-  // 8 MiB vectors needs that memory-level parallelism from 2 CTAs per SM (the partial-sum CTAs)
-  constexpr int kU = 4;
   constexpr int NY = comb_inputs(KIND);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < a.m; i0 += kU * stride) {
-    double xv[kU], yv[NY > 0 ? NY : 1][kU], ov[kU];
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int64_t i = i0 + q * stride < a.m ? i0 + q * stride : i0;  // clamped: unpredicated loads
-      xv[q] = x[i];
-#pragma unroll
-      for (int j = 0; j < NY; ++j) yv[j][q] = a.y[comb_slot(KIND, j)][i];
-      ov[q] = (RED && KIND != C_F_OUT && a.other) ? a.other[i] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const int64_t i = i0 + q * stride;
-      if (i >= a.m) break;
-      const double xi = xv[q];
-      double o, other = 0.0;
-      using namespace rkf;
-      switch (KIND) {
-        case C_RK2_ST: o = xi + t * yv[0][q]; break;
-        case C_RK2_OUT: o = xi + 0.5 * t * (yv[0][q] + yv[1][q]); break;
-        case C_RK4_STH: o = xi + 0.5 * t * yv[0][q]; break;
-        case C_RK4_ST1: o = xi + t * yv[0][q]; break;
-        case C_RK4_OUT: o = xi + t * (yv[0][q] + 2.0 * yv[1][q] + 2.0 * yv[2][q] + yv[3][q]) / 6.0; break;
-        case C_F2: o = xi + t * a21 * yv[0][q]; break;
-        case C_F3: o = xi + t * (a31 * yv[0][q] + a32 * yv[1][q]); break;
-        case C_F4: o = xi + t * (a41 * yv[0][q] + a42 * yv[1][q] + a43 * yv[2][q]); break;
-        case C_F5: o = xi + t * (a51 * yv[0][q] + a52 * yv[1][q] + a53 * yv[2][q] + a54 * yv[3][q]); break;
-        case C_F6:
-          o = xi + t * (a61 * yv[0][q] + a62 * yv[1][q] + a63 * yv[2][q] + a64 * yv[3][q] + a65 * yv[4][q]);
-          break;
-        default: {  // C_F_OUT: inputs k1, k3, k4, k5, k6
-          const double k1 = yv[0][q], k3 = yv[1][q], k4 = yv[2][q], k5 = yv[3][q], k6 = yv[4][q];
-          other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
-          o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
-          if (store5) a.n5[i] = other;
-          break;
-        }
+  // one element: the stage combination, its store, and the fused reductions of the final pass
+  auto elem = [&](int64_t i, double xi, const double* yy, double ovi) {
+    double o, other = 0.0;
+    using namespace rkf;
+    switch (KIND) {
+      case C_RK2_ST: o = xi + t * yy[0]; break;
+      case C_RK2_OUT: o = xi + 0.5 * t * (yy[0] + yy[1]); break;
+      case C_RK4_STH: o = xi + 0.5 * t * yy[0]; break;
+      case C_RK4_ST1: o = xi + t * yy[0]; break;
+      case C_RK4_OUT: o = xi + t * (yy[0] + 2.0 * yy[1] + 2.0 * yy[2] + yy[3]) / 6.0; break;
+      case C_F2: o = xi + t * a21 * yy[0]; break;
+      case C_F3: o = xi + t * (a31 * yy[0] + a32 * yy[1]); break;
+      case C_F4: o = xi + t * (a41 * yy[0] + a42 * yy[1] + a43 * yy[2]); break;
+      case C_F5: o = xi + t * (a51 * yy[0] + a52 * yy[1] + a53 * yy[2] + a54 * yy[3]); break;
+      case C_F6: o = xi + t * (a61 * yy[0] + a62 * yy[1] + a63 * yy[2] + a64 * yy[3] + a65 * yy[4]); break;
+      default: {  // C_F_OUT: inputs k1, k3, k4, k5, k6
+        const double k1 = yy[0], k3 = yy[1], k4 = yy[2], k5 = yy[3], k6 = yy[4];
+        other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
+        o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
+        if (store5) a.n5[i] = other;
+        break;
       }
-      out[i] = o;
-      if (RED) {
-        if (KIND != C_F_OUT && a.other) other = ov[q];
-        if (KIND == C_F_OUT || a.other) {
-          const double d = o - other;
-          acc[RF_ERR2] += d * d;
-          if (!finite_d(other)) acc[RF_NF_OTHER] = 1.0;
+    }
+    out[i] = o;
+    if (RED) {
+      if (KIND != C_F_OUT && a.other) other = ovi;
+      if (KIND == C_F_OUT || a.other) {
+        const double d = o - other;
+        acc[RF_ERR2] += d * d;
+        if (!finite_d(other)) acc[RF_NF_OTHER] = 1.0;
+      }
+      if (!finite_d(o)) acc[RF_NF_CAND] = 1.0;
+      const double kk = (double)(i + 1);
+      acc[RF_L2SQ] += o * o;
+      acc[RF_MOM0] += o;
+      acc[RF_MOM1] += kk * o;
+      acc[RF_MOM2] += kk * kk * o;
+      acc[RF_MIN] = o < acc[RF_MIN] ? o : acc[RF_MIN];
+      const double ab = fabs(o);
+      acc[RF_MAXABS] = acc[RF_MAXABS] < ab ? ab : acc[RF_MAXABS];
+    }
+  };
+  // kU element pairs (16-byte loads) per thread per step, all loads issued before any
+  // arithmetic: a pass over 8 MiB vectors needs that memory-level parallelism from 2 CTAs per SM
+  // (the partial-sum CTAs). Odd m: the same with single elements.
+  constexpr int kU = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const bool want_other = RED && KIND != C_F_OUT && a.other;
+  if ((a.m & 1) == 0) {
+    const int64_t mp = a.m / 2;
+    auto ld2 = [](const double* p, int64_t k) { return reinterpret_cast<const double2*>(p)[k]; };
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < mp; i0 += kU * stride) {
+      double2 xv[kU], yv[NY][kU], ov[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int64_t k = i0 + q * stride < mp ? i0 + q * stride : i0;  // clamped: unpredicated loads
+        xv[q] = ld2(x, k);
+#pragma unroll
+        for (int j = 0; j < NY; ++j) yv[j][q] = ld2(a.y[comb_slot(KIND, j)], k);
+        ov[q] = want_other ? ld2(a.other, k) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int64_t k = i0 + q * stride;
+        if (k >= mp) break;
+        double y0[NY], y1[NY];
+#pragma unroll
+        for (int j = 0; j < NY; ++j) {
+          y0[j] = yv[j][q].x;
+          y1[j] = yv[j][q].y;
         }
-        if (!finite_d(o)) acc[RF_NF_CAND] = 1.0;
-        const double kk = (double)(i + 1);
-        acc[RF_L2SQ] += o * o;
-        acc[RF_MOM0] += o;
-        acc[RF_MOM1] += kk * o;
-        acc[RF_MOM2] += kk * kk * o;
-        acc[RF_MIN] = o < acc[RF_MIN] ? o : acc[RF_MIN];
-        const double ab = fabs(o);
-        acc[RF_MAXABS] = acc[RF_MAXABS] < ab ? ab : acc[RF_MAXABS];
+        elem(2 * k, xv[q].x, y0, ov[q].x);
+        elem(2 * k + 1, xv[q].y, y1, ov[q].y);
+      }
+    }
+  } else {
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < a.m; i0 += kU * stride) {
+      double xv[kU], yv[NY][kU], ov[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int64_t i = i0 + q * stride < a.m ? i0 + q * stride : i0;
+        xv[q] = x[i];
+#pragma unroll
+        for (int j = 0; j < NY; ++j) yv[j][q] = a.y[comb_slot(KIND, j)][i];
+        ov[q] = want_other ? a.other[i] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const int64_t i = i0 + q * stride;
+        if (i >= a.m) break;
+        double yy[NY];
+#pragma unroll
+        for (int j = 0; j < NY; ++j) yy[j] = yv[j][q];
+        elem(i, xv[q], yy, ov[q]);
       }
     }
   }
