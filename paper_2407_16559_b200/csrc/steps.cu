@@ -96,8 +96,10 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
   }
   constexpr int NY = comb_inputs(KIND);
   // one element: the stage combination, its store, and the fused reductions of the final pass
-  auto elem = [&](int64_t i, double xi, const double* yy, double ovi) {
-    double o, other = 0.0;
+  // returns the output value o; the caller stores it (and n5 = `other` for C_F_OUT)
+  auto elem = [&](int64_t i, double xi, const double* yy, double ovi, double& other) -> double {
+    double o;
+    other = 0.0;
     using namespace rkf;
     switch (KIND) {
       case C_RK2_ST: o = xi + t * yy[0]; break;
@@ -114,11 +116,10 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
         const double k1 = yy[0], k3 = yy[1], k4 = yy[2], k5 = yy[3], k6 = yy[4];
         other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
         o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
-        if (store5) a.n5[i] = other;
         break;
       }
     }
-    out[i] = o;
+    const double n5v = other;
     if (RED) {
       if (KIND != C_F_OUT && a.other) other = ovi;
       if (KIND == C_F_OUT || a.other) {
@@ -136,6 +137,8 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
       const double ab = fabs(o);
       acc[RF_MAXABS] = acc[RF_MAXABS] < ab ? ab : acc[RF_MAXABS];
     }
+    other = n5v;
+    return o;
   };
   // kU element pairs (16-byte loads) per thread per step, all loads issued before any
   // arithmetic: a pass over 8 MiB vectors needs that memory-level parallelism from 2 CTAs per SM
@@ -166,8 +169,11 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
           y0[j] = yv[j][q].x;
           y1[j] = yv[j][q].y;
         }
-        elem(2 * k, xv[q].x, y0, ov[q].x);
-        elem(2 * k + 1, xv[q].y, y1, ov[q].y);
+        double f0, f1;
+        const double o0 = elem(2 * k, xv[q].x, y0, ov[q].x, f0);
+        const double o1 = elem(2 * k + 1, xv[q].y, y1, ov[q].y, f1);
+        reinterpret_cast<double2*>(out)[k] = make_double2(o0, o1);
+        if (store5) reinterpret_cast<double2*>(a.n5)[k] = make_double2(f0, f1);
       }
     }
   } else {
@@ -188,7 +194,9 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
         double yy[NY];
 #pragma unroll
         for (int j = 0; j < NY; ++j) yy[j] = yv[j][q];
-        elem(i, xv[q], yy, ov[q]);
+        double f0;
+        out[i] = elem(i, xv[q], yy, ov[q], f0);
+        if (store5) a.n5[i] = f0;
       }
     }
   }
