@@ -20,10 +20,32 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 #include "steps.cuh"
 
 using namespace agk;
+
+namespace {
+// NVTX range around each C-ABI entry point (domain "agk"): host-side API spans for a timeline
+// tool; header-only NVTX v3, a no-op pointer check when no tool is attached.
+struct NvtxRange {
+  static nvtxDomainHandle_t domain() {
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("agk");
+    return d;
+  }
+  explicit NvtxRange(const char* name) {
+    nvtxEventAttributes_t a = {};
+    a.version = NVTX_VERSION;
+    a.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    a.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    a.message.ascii = name;
+    nvtxDomainRangePushEx(domain(), &a);
+  }
+  ~NvtxRange() { nvtxDomainRangePop(domain()); }
+};
+}  // namespace
 
 struct agk_rhs {
   int device = 0;
@@ -364,6 +386,7 @@ const char* agk_describe_status(int s) {
 const char* agk_last_error(const agk_rhs* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
 
 agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
+  NvtxRange nvtx_("agk_rhs_create");
   if (!d || !out) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "null argument");
   *out = nullptr;
   // ModelSpec::validate (rhs.cpp:63-72) and SourceTerm::validate (rhs.cpp:48-61)
@@ -661,6 +684,7 @@ void agk_rhs_reset_evals(agk_rhs* h) {
 int agk_rhs_launches_per_eval(const agk_rhs* h) { return h ? (h->kind == AGK_RHS_MODEL ? h->plan.launches : 1) : 0; }
 
 agk_status agk_rhs_eval(agk_rhs* h, const double* n, double* out, int where) {
+  NvtxRange nvtx_("agk_rhs_eval");
   if (!h) return fail(nullptr, AGK_ERR_INVALID_ARGUMENT, "null handle");
   if (h->kind != AGK_RHS_MODEL) {
     DeviceGuard dg(h->device);
@@ -771,6 +795,7 @@ static agk_status advance_impl(agk_rhs* h, const double* n, double tau, const ag
 
 agk_status agk_advance(agk_rhs* h, const double* n, double tau, const agk_control* c, agk_outcome* o,
                        double* state_out, int where) {
+  NvtxRange nvtx_("agk_advance");
   if (!h || !n || !c || !o) return fail(h, AGK_ERR_INVALID_ARGUMENT, "null argument");
   if (c->stepper < 0 || c->stepper > 2 || c->mode < 0 || c->mode > 1)
     return fail(h, AGK_ERR_INVALID_ARGUMENT, "unknown stepper or mode");
@@ -780,6 +805,7 @@ agk_status agk_advance(agk_rhs* h, const double* n, double tau, const agk_contro
 
 agk_status agk_rk_step(agk_rhs* h, int stepper, const double* n, double tau, double* out, double* out5, double* err,
                        int where) {
+  NvtxRange nvtx_("agk_rk_step");
   if (!h || !n || !out) return fail(h, AGK_ERR_INVALID_ARGUMENT, "null argument");
   if (stepper < 0 || stepper > 2) return fail(h, AGK_ERR_INVALID_ARGUMENT, "unknown stepper");
   if (!(tau > 0.0)) return fail(h, AGK_ERR_INVALID_ARGUMENT, "step size must be > 0");
@@ -801,6 +827,7 @@ agk_status agk_rk_step(agk_rhs* h, int stepper, const double* n, double tau, dou
 }
 
 agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
+  NvtxRange nvtx_("agk_run");
   if (!h || !d || !rep) return fail(h, AGK_ERR_INVALID_ARGUMENT, "null argument");
   if (h->kind != AGK_RHS_MODEL) return fail(h, AGK_ERR_INVALID_ARGUMENT, "run() drives the model right-hand side");
   // SimulationConfig::validate (simulator.cpp:23-49)
