@@ -57,7 +57,20 @@ def parse():
     ap.add_argument("--ref-budget-s", type=float, default=240.0)
     ap.add_argument("--adaptive-horizon", type=float, default=200.0,
                     help="config-5 RKF45 adaptive solve to this t (0: skip); t_end is 1e5")
+    ap.add_argument("--no-t-end", action="store_true", help="skip the time-to-t_end legs (configs 1, 2)")
     return ap.parse_args()
+
+
+def spawn_replicas(args):
+    """--gpus N without a torchrun environment: launch the N replicas ourselves (one process per
+    GPU, the same torch.distributed.run command the driver uses) and pass their exit code on."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ distributed plumbing
@@ -376,6 +389,8 @@ def run_b200(args, world, rank, local):
     ws.close()
     if args.adaptive_horizon > 0:
         res["adaptive"] = adaptive_leg(args, world, local)
+    if not args.no_t_end:
+        res["t_end"] = t_end_legs(args, world, rank, local)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         res["cpu_baseline"] = cpu_baseline_sample(U, V, n)
     return res
@@ -407,9 +422,74 @@ def adaptive_leg(args, world, local):
             "us_per_rhs_in_run": 1e6 * wall / max(rep.total_rhs_evals, 1)}
 
 
+def t_end_legs(args, world, rank, local):
+    """Time to t_end (the metric's second half) on full BASELINE configs, each beside the
+    reference's own CPU run() on this box's host (oracle/_ref, one core: run() is single-threaded):
+      * config 1 (M=4096, constant kernel, t_end=100) with each of the three schemes: GPU and CPU
+        both measured in full;
+      * config 2 (M=2^16, Brownian+2 with a monomer source, n0=0, t_end=1e4) RKF45: GPU in full;
+        the CPU time is EXTRAPOLATED as (measured CPU seconds per RHS at this shape) x (the run's
+        RHS count), since the full CPU run takes hours.
+    GPU wall time is around agk.run (graph built by a first short run), device-resident."""
+    import torch
+    import paper_2407_16559_b200 as agk
+    from paper_2407_16559_b200.configs import baseline_config
+    try:
+        from oracle.oracle import Control as OC, Model as OM, Oracle
+        ref = Oracle("reference")
+    except Exception:
+        ref = None
+    legs = []
+    for idx, schemes in ((1, (agk.RK2, agk.RK4, agk.RKF45)), (2, (agk.RKF45,))):
+        cfg = baseline_config(idx)
+        ws = agk.RhsWorkspace(agk.Model(cfg["u"], cfg["v"], cfg["variant"], cfg["sources"], cfg["lam"]),
+                              device=local)
+        for st in schemes:
+            ctl = agk.StepControl(stepper=st, tol=cfg["tol"])
+            agk.run(ws, agk.SimulationConfig(ctl, min(cfg["t_end"], 1e-3), cfg["n0"]))  # graph build
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = agk.run(ws, agk.SimulationConfig(ctl, cfg["t_end"], cfg["n0"]))
+            wall = max_over_ranks(time.perf_counter() - t0, world, local)
+            leg = {"config": idx, "scheme": ("rk2", "rk4", "rkf45")[st], "t_end": cfg["t_end"],
+                   "m": int(cfg["n0"].size), "termination": rep.termination, "final_t": rep.final_t,
+                   "gpu_wall_s": wall, "accepted": rep.total_accepted, "rejects": rep.total_rejects,
+                   "rhs_evals": rep.total_rhs_evals, "accepted_steps_per_s": world * rep.total_accepted / wall,
+                   "us_per_rhs_in_run": 1e6 * wall / max(rep.total_rhs_evals, 1)}
+            if ref is not None and rank == 0:
+                md = OM(cfg["u"], cfg["v"], cfg["variant"], list(cfg["sources"]), cfg["lam"])
+                if idx == 1:
+                    t0 = time.perf_counter()
+                    w = ref.run(md, cfg["n0"], OC(stepper=st, tol=cfg["tol"]), cfg["t_end"])
+                    cpu = time.perf_counter() - t0
+                    leg["cpu_reference"] = {"wall_s": cpu, "kind": "measured", "cores": 1,
+                                            "accepted": w["total_accepted"], "rhs_evals": w["total_rhs_evals"]}
+                else:
+                    k = 20
+                    x = np.abs(np.random.default_rng(1).standard_normal(cfg["n0"].size)) * 1e-3
+                    ref.eval_rhs(md, x)
+                    t0 = time.perf_counter()
+                    for _ in range(k):
+                        ref.eval_rhs(md, x)
+                    per = (time.perf_counter() - t0) / k
+                    leg["cpu_reference"] = {"wall_s": per * rep.total_rhs_evals, "kind": "extrapolated", "cores": 1,
+                                            "s_per_rhs": per, "sample": f"{k} eval_rhs at this shape x the GPU "
+                                                                        "run's RHS count"}
+                leg["speedup_vs_cpu"] = leg["cpu_reference"]["wall_s"] / wall
+            legs.append(leg)
+        ws.close()
+    return legs
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_replicas(args))
     world, rank, local = dist_setup()
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting the true rank count",
+              file=sys.stderr)
     if args.impl == "reference":
         res = run_reference(args, world, rank)
     else:

@@ -10,7 +10,15 @@
  * buffers, one CUDA stream and its captured graphs. Calls on different handles may run
  * concurrently from different host threads; one handle must not be used by two threads at
  * once. Errors: an agk_status, and agk_last_error(handle) for the message (the reference
- * throws std::invalid_argument with the same conditions).
+ * throws std::invalid_argument with the same conditions). No entry point changes the calling
+ * thread's current CUDA device.
+ *
+ * Stream ordering of device pointers (AGK_MEM_DEVICE): the handle's stream is a BLOCKING
+ * stream, so it is ordered after all work previously queued on the legacy default stream
+ * (stream 0, e.g. torch's default stream) and that stream waits for it. Inputs produced on any
+ * other stream must be complete before the call (synchronize that stream or record/wait an
+ * event); the paper_2407_16559_b200 Python wrapper synchronizes torch's current stream for CUDA
+ * tensors. Every call except agk_rhs_eval_async returns after its outputs are written.
  */
 #ifndef AGK_AGK_H
 #define AGK_AGK_H
@@ -22,7 +30,7 @@
 extern "C" {
 #endif
 
-#define AGK_ABI_VERSION 2
+#define AGK_ABI_VERSION 3
 
 typedef enum {
   AGK_OK = 0,
@@ -162,6 +170,12 @@ typedef struct {
   uint64_t rhs_evals, rejects;
 } agk_record;
 
+/* Record stream (ABI 3): called on the calling thread, in order, with every record the run
+ * produces, the closing record (simulator.cpp:219-222) included. The device keeps records in
+ * a ring buffer and pauses the WHILE graph to drain it into the sink, so no record is dropped
+ * whatever the run length (the reference RunReport keeps them all, simulator.cpp:130-145). */
+typedef void (*agk_record_sink)(void* user, const agk_record* recs, size_t n);
+
 /* RunReport (simulator.hpp:52-64). Caller-provided buffers may be NULL. */
 typedef struct {
   int termination;           /* 0 completed, 1 aborted */
@@ -175,7 +189,9 @@ typedef struct {
   size_t num_snapshots_taken;
   agk_record* records;       /* in: host buffer, or NULL */
   size_t records_capacity;
-  size_t num_records;        /* produced; only the first records_capacity are stored */
+  size_t num_records;        /* produced; the first records_capacity are also stored in records */
+  agk_record_sink record_sink; /* in: receives every record (ABI 3), or NULL */
+  void* sink_user;
 } agk_run_report;
 
 /* run (simulator.cpp:112-229): the whole integration runs as one device-resident CUDA graph

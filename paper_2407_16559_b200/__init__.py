@@ -74,12 +74,18 @@ class _Record(C.Structure):
                 ("rejects", C.c_uint64)]
 
 
+_RecordSink = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(_Record), C.c_size_t)
+RECORD_DTYPE = np.dtype([("t", "<f8"), ("tau", "<f8"), ("density", "<f8"), ("mass", "<f8"), ("m2", "<f8"),
+                         ("error_estimate", "<f8"), ("rhs_evals", "<u8"), ("rejects", "<u8")])
+
+
 class _Report(C.Structure):
     _fields_ = [("termination", C.c_int), ("abort_status", C.c_int), ("abort_t", C.c_double),
                 ("abort_tau", C.c_double), ("final_t", C.c_double), ("total_rhs_evals", C.c_uint64),
                 ("total_accepted", C.c_uint64), ("total_rejects", C.c_uint64), ("wall_seconds", C.c_double),
                 ("final_state", _dp), ("snapshots", _dp), ("num_snapshots_taken", C.c_size_t),
-                ("records", C.POINTER(_Record)), ("records_capacity", C.c_size_t), ("num_records", C.c_size_t)]
+                ("records", C.POINTER(_Record)), ("records_capacity", C.c_size_t), ("num_records", C.c_size_t),
+                ("record_sink", _RecordSink), ("sink_user", C.c_void_p)]
 
 
 # exported symbols and their signatures (must match include/agk/agk.h)
@@ -152,13 +158,18 @@ def describe(status: int) -> str:
 # ---------------------------------------------------------------------------- arrays
 
 class _Arr:
-    """Host numpy or CUDA torch array as (pointer, where, keepalive)."""
+    """Host numpy or CUDA torch array as (pointer, where, keepalive).
+
+    CUDA tensors: torch's current stream is synchronized first, so a tensor whose producing kernel
+    (or, for outputs, whose previous user) is still queued is complete before the handle's stream
+    touches it (the handle's stream is only ordered after the legacy default stream, agk.h)."""
 
     def __init__(self, x, m, writable=False):
         if hasattr(x, "is_cuda") and x.is_cuda:
             import torch
             if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != m:
                 raise ValueError("device arrays must be contiguous float64 of size m")
+            torch.cuda.current_stream(x.device).synchronize()
             self.ptr, self.where, self.obj = x.data_ptr(), MEM_DEVICE, x
         else:
             a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).reshape(-1))
@@ -425,7 +436,6 @@ class SimulationConfig:
     snapshot_times: Sequence[float] = ()
     record: int = RECORD_NONE
     record_interval: float = 0.0
-    records_capacity: int = 0
 
 
 @dataclass
@@ -455,21 +465,24 @@ def run(ws: RhsWorkspace, cfg: SimulationConfig) -> RunReport:
     st_buf = st if st.size else np.zeros(1)
     final = np.zeros(m)
     snaps = np.zeros((max(st.size, 1), m))
-    cap = cfg.records_capacity
-    if cfg.record != RECORD_NONE and cap == 0:
-        cap = 4096
-    recs = (_Record * max(cap, 1))()
     d = _RunDesc(cfg.control.c(), float(cfg.t_end), init.ctypes.data_as(_dp), float(cfg.initial_tau),
                  st_buf.ctypes.data_as(_dp), st.size, cfg.record, float(cfg.record_interval))
     rep = _Report()
     rep.final_state = final.ctypes.data_as(_dp)
     rep.snapshots = snaps.ctypes.data_as(_dp)
-    rep.records = recs
-    rep.records_capacity = cap
+    # every record streams through the sink (the device drains its record ring between segments)
+    chunks = []
+
+    def _sink(_user, recs, n):
+        chunks.append(np.ctypeslib.as_array(C.cast(recs, C.POINTER(C.c_uint8)), shape=(n * RECORD_DTYPE.itemsize,))
+                      .view(RECORD_DTYPE).copy())
+
+    sink = _RecordSink(_sink)
+    if cfg.record != RECORD_NONE:
+        rep.record_sink = sink
     _check(load_library().agk_run(ws.handle, C.byref(d), C.byref(rep)), ws.handle)
-    nrec = min(rep.num_records, cap)
-    records = [dict(t=r.t, tau=r.tau, density=r.density, mass=r.mass, m2=r.m2, error_estimate=r.error_estimate,
-                    rhs_evals=r.rhs_evals, rejects=r.rejects) for r in recs[:nrec]]
+    arr = np.concatenate(chunks) if chunks else np.zeros(0, dtype=RECORD_DTYPE)
+    records = [dict(zip(RECORD_DTYPE.names, row)) for row in arr.tolist()]
     snapshots = [(float(st[q]), snaps[q].copy()) for q in range(rep.num_snapshots_taken)]
     return RunReport("completed" if rep.termination == 0 else "aborted",
                      "" if rep.termination == 0 else describe(rep.abort_status), rep.abort_t, rep.abort_tau,

@@ -11,6 +11,7 @@
 // reference's bitwise comparison rule.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -76,6 +77,8 @@ struct agk_rhs {
   const double* rhs_graph_in = nullptr;
   double* rhs_graph_out = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  agk_record* rec_ring = nullptr;  // device record ring of agk_run (allocated on first use)
+  ~agk_rhs();
 };
 
 namespace {
@@ -134,9 +137,7 @@ agk_status select_device(agk_rhs* h, int device) {
   if (e != cudaSuccess) return cuda_fail(h, e, "cudaGetDeviceProperties");
   if (prop.major < 10)
     return fail(h, AGK_ERR_NO_DEVICE, std::string("device ") + prop.name + " is not sm_100: kernels are built for sm_100a only");
-  e = cudaSetDevice(device);
-  if (e != cudaSuccess) return cuda_fail(h, e, "cudaSetDevice");
-  h->device = device;
+  h->device = device;  // made current only inside each call (DeviceGuard)
   return AGK_OK;
 }
 
@@ -153,9 +154,28 @@ struct DeviceGuard {
   }
 };
 
+}  // namespace
+
+// Releases everything the handle owns (also on a failed create: unique_ptr<agk_rhs>).
+agk_rhs::~agk_rhs() {
+  DeviceGuard dg(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  if (rhs_graph) cudaGraphExecDestroy(rhs_graph);
+  if (rhs_graph_b) cudaGraphExecDestroy(rhs_graph_b);
+  for (void* p : allocs) cudaFree(p);
+  if (ev0) cudaEventDestroy(ev0);
+  if (ev1) cudaEventDestroy(ev1);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
 agk_status alloc_common(agk_rhs* h) {
   const int64_t m = h->m;
-  CK_H(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+  // blocking stream: ordered after (and before) work on the legacy default stream, so device
+  // inputs produced there (torch's default stream) are complete when a kernel reads them
+  CK_H(h, cudaStreamCreateWithFlags(&h->stream, cudaStreamDefault), "cudaStreamCreate");
   CK_H(h, cudaEventCreate(&h->ev0), "cudaEventCreate");
   CK_H(h, cudaEventCreate(&h->ev1), "cudaEventCreate");
   CK_H(h, dalloc(h, &h->d_in, m), "alloc in");
@@ -412,6 +432,7 @@ agk_status agk_rhs_create(const agk_model_desc* d, agk_rhs** out) {
     g_create_error = h->err;
     return st;
   }
+  DeviceGuard dg(h->device);  // restores the caller's current device on every return path
   if (d->k) return create_dense(d, std::move(h), out);
   const int64_t m = (int64_t)d->m;
   const int r = (int)d->r;
@@ -646,6 +667,7 @@ agk_status agk_rhs_create_fake(int kind, size_t m, double param, int device, agk
     g_create_error = h->err;
     return st;
   }
+  DeviceGuard dg(h->device);
   h->kind = kind;
   h->fake_param = param;
   h->m = (int64_t)m;
@@ -661,19 +683,7 @@ agk_status agk_rhs_create_fake(int kind, size_t m, double param, int device, agk
   return AGK_OK;
 }
 
-void agk_rhs_destroy(agk_rhs* h) {
-  if (!h) return;
-  DeviceGuard dg(h->device);
-  cudaStreamSynchronize(h->stream);
-  for (auto& kv : h->graphs) cudaGraphExecDestroy(kv.second);
-  if (h->rhs_graph) cudaGraphExecDestroy(h->rhs_graph);
-  if (h->rhs_graph_b) cudaGraphExecDestroy(h->rhs_graph_b);
-  for (void* p : h->allocs) cudaFree(p);
-  if (h->ev0) cudaEventDestroy(h->ev0);
-  if (h->ev1) cudaEventDestroy(h->ev1);
-  if (h->stream) cudaStreamDestroy(h->stream);
-  delete h;
-}
+void agk_rhs_destroy(agk_rhs* h) { delete h; }
 
 size_t agk_rhs_size(const agk_rhs* h) { return h ? (size_t)h->m : 0; }
 size_t agk_rhs_unique_ranks(const agk_rhs* h) { return h ? (size_t)h->rf : 0; }
@@ -854,32 +864,32 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
   agk_status st = get_graph(h, body, d->control.stepper, &ex);
   if (st) return st;
   const int64_t m = h->m;
+  // per-run device buffers, freed on every return path
+  struct TmpBufs {
+    std::vector<void*> p;
+    ~TmpBufs() {
+      for (void* q : p) cudaFree(q);
+    }
+  } tmp;
   double* snap_times = nullptr;
   double* snap_buf = nullptr;
-  agk_record* rec_buf = nullptr;
-  std::vector<void*> tmp;
-  auto release = [&]() {
-    for (void* p : tmp) cudaFree(p);
-  };
   if (d->num_snapshots) {
     CK_H(h, cudaMalloc(&snap_times, d->num_snapshots * sizeof(double)), "alloc snapshots");
-    tmp.push_back(snap_times);
+    tmp.p.push_back(snap_times);
     CK_H(h, cudaMemcpyAsync(snap_times, d->snapshot_times, d->num_snapshots * sizeof(double), cudaMemcpyHostToDevice,
                             h->stream), "upload snapshots");
     if (rep->snapshots) {
       CK_H(h, cudaMalloc(&snap_buf, d->num_snapshots * m * sizeof(double)), "alloc snapshot buffer");
-      tmp.push_back(snap_buf);
+      tmp.p.push_back(snap_buf);
     }
   }
-  if (rep->records && rep->records_capacity && d->record != AGK_RECORD_NONE) {
-    CK_H(h, cudaMalloc(&rec_buf, rep->records_capacity * sizeof(agk_record)), "alloc records");
-    tmp.push_back(rec_buf);
-  }
+  // records: a device ring of kRing records, drained to the host whenever it fills (the
+  // controller then leaves the WHILE loop with `paused`, the graph is relaunched in resume mode)
+  constexpr int64_t kRing = 1 << 16;
+  const bool want_rec = d->record != AGK_RECORD_NONE && (rep->record_sink || (rep->records && rep->records_capacity));
+  if (want_rec && !h->rec_ring) CK_H(h, dalloc(h, &h->rec_ring, (size_t)kRing), "alloc record ring");
   st = copy_in(h, d->initial, AGK_MEM_HOST, h->sb.state);
-  if (st) {
-    release();
-    return st;
-  }
+  if (st) return st;
   DevCtl c{};
   control_to_ctl(&d->control, &c);
   c.run_mode = RUN_LOOP;
@@ -890,18 +900,46 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
   c.snap_buf = snap_buf;
   c.record = d->record;
   c.record_interval = d->record_interval;
-  c.rec_buf = rec_buf;
-  c.rec_cap = rec_buf ? (int64_t)rep->records_capacity : 0;
+  c.rec_buf = want_rec ? h->rec_ring : nullptr;
+  c.rec_cap = want_rec ? kRing : 0;
   c.has_model = 1;
   c.cur = 0;
   CK_H(h, cudaMemcpyAsync(h->ctl, &c, sizeof(DevCtl), cudaMemcpyHostToDevice, h->stream), "ctl upload");
-  CK_H(h, cudaGraphLaunch(ex, h->stream), "graph launch");
+  size_t delivered = 0;  // records handed to the caller so far
+  std::vector<agk_record> chunk;
+  auto deliver = [&](const agk_record* r, size_t n) {
+    if (!n) return;
+    if (rep->records) {
+      for (size_t q = 0; q < n && delivered + q < rep->records_capacity; ++q) rep->records[delivered + q] = r[q];
+    }
+    if (rep->record_sink) rep->record_sink(rep->sink_user, r, n);
+    delivered += n;
+  };
   DevCtl r;
-  CK_H(h, cudaMemcpyAsync(&r, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream), "ctl download");
-  cudaError_t e = cudaStreamSynchronize(h->stream);
-  if (e != cudaSuccess) {
-    release();
-    return cuda_fail(h, e, "run");
+  for (;;) {
+    CK_H(h, cudaGraphLaunch(ex, h->stream), "graph launch");
+    CK_H(h, cudaMemcpyAsync(&r, h->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, h->stream), "ctl download");
+    CK_H(h, cudaStreamSynchronize(h->stream), "run");
+    if (want_rec) {
+      // drain [rec_drained, nrec) of the ring (one or two contiguous pieces)
+      const long long from = r.rec_drained, to = r.nrec;
+      chunk.resize((size_t)(to - from));
+      for (long long q = from; q < to;) {
+        const long long slot = q % kRing, n = std::min<long long>(to - q, kRing - slot);
+        CK_H(h, cudaMemcpyAsync(chunk.data() + (q - from), h->rec_ring + slot, (size_t)n * sizeof(agk_record),
+                                cudaMemcpyDeviceToHost, h->stream), "copy records");
+        q += n;
+      }
+      CK_H(h, cudaStreamSynchronize(h->stream), "copy records");
+      deliver(chunk.data(), chunk.size());
+    }
+    if (!r.paused) break;
+    // resume: the loop state stays on the device; only the drain mark and the resume flag change
+    const long long drained = r.nrec;
+    const int one = 1;
+    CK_H(h, cudaMemcpyAsync(&h->ctl->rec_drained, &drained, sizeof(drained), cudaMemcpyHostToDevice, h->stream),
+         "ctl update");
+    CK_H(h, cudaMemcpyAsync(&h->ctl->resume, &one, sizeof(one), cudaMemcpyHostToDevice, h->stream), "ctl update");
   }
   rep->termination = r.status == AGK_STEP_OK ? 0 : 1;
   rep->abort_status = r.status;
@@ -911,7 +949,6 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
   rep->total_rhs_evals = r.evals;
   rep->total_accepted = r.accepted;
   rep->total_rejects = r.rejects_total;
-  size_t nrec = (size_t)r.nrec;
   if (rep->final_state)
     CK_H(h, cudaMemcpyAsync(rep->final_state, h->sb.state + (int64_t)r.cur * m, m * sizeof(double),
                             cudaMemcpyDeviceToHost, h->stream), "copy final state");
@@ -919,36 +956,21 @@ agk_status agk_run(agk_rhs* h, const agk_run_desc* d, agk_run_report* rep) {
   if (snap_buf && r.snap_idx > 0)
     CK_H(h, cudaMemcpyAsync(rep->snapshots, snap_buf, (size_t)r.snap_idx * m * sizeof(double), cudaMemcpyDeviceToHost,
                             h->stream), "copy snapshots");
-  if (rec_buf) {
-    const size_t ncopy = nrec < rep->records_capacity ? nrec : rep->records_capacity;
-    if (ncopy)
-      CK_H(h, cudaMemcpyAsync(rep->records, rec_buf, ncopy * sizeof(agk_record), cudaMemcpyDeviceToHost, h->stream),
-           "copy records");
-  }
-  e = cudaStreamSynchronize(h->stream);
-  release();
-  if (e != cudaSuccess) return cuda_fail(h, e, "run copy-out");
-  // closing record (simulator.cpp:219-222)
-  if (d->record != AGK_RECORD_NONE && rep->termination == 0) {
-    bool need = nrec == 0;
-    if (!need) {
-      const size_t last = nrec - 1;
-      need = (rep->records && last < rep->records_capacity) ? rep->records[last].t < r.t : false;
-    }
-    if (need) {
-      if (rep->records && nrec < rep->records_capacity) {
-        agk_record& x = rep->records[nrec];
-        x.t = r.t;
-        x.tau = 0.0;
-        x.density = r.mom[0];
-        x.mass = r.mom[1];
-        x.m2 = r.mom[2];
-        x.error_estimate = NAN;
-        x.rhs_evals = r.evals;
-        x.rejects = r.rejects_total;
-      }
-      nrec += 1;
-    }
+  CK_H(h, cudaStreamSynchronize(h->stream), "run copy-out");
+  size_t nrec = (size_t)r.nrec;
+  // closing record (simulator.cpp:219-222): when the run completed and the last record is not at t
+  if (d->record != AGK_RECORD_NONE && rep->termination == 0 && (nrec == 0 || r.last_rec_t < r.t)) {
+    agk_record x{};
+    x.t = r.t;
+    x.tau = 0.0;
+    x.density = r.mom[0];
+    x.mass = r.mom[1];
+    x.m2 = r.mom[2];
+    x.error_estimate = NAN;
+    x.rhs_evals = r.evals;
+    x.rejects = r.rejects_total;
+    if (want_rec) deliver(&x, 1);
+    nrec += 1;
   }
   rep->num_records = nrec;
   h->evals += r.evals;

@@ -100,6 +100,16 @@ enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANS
 // pdl_entry()/griddepcontrol.wait before anything written by earlier launches, and triggers its
 // own dependents only after that wait — so a dependent overlaps its immediate predecessor only.
 // AGK_PDL=0 turns it off (ordinary stream serialisation); per-kernel timing marks also do.
+// Experiment knobs (tools/ab.sh, tools/timeline.py, tools/tune.py): read from the environment
+// ONLY in a library built with -DAGK_EXPERIMENTS (`make EXPERIMENTS=1`). The production library
+// ignores the environment entirely, so no stray variable can change the plan or skip work.
+#ifdef AGK_EXPERIMENTS
+int knob(const char* name, int dflt);
+#define AGK_XDBG(a, bits) (((a).dbg & (bits)) != 0)
+#else
+inline int knob(const char*, int dflt) { return dflt; }
+#define AGK_XDBG(a, bits) false
+#endif
 bool pdl_enabled();
 int pdl_mask();  // AGK_PDLMASK experiment bits (default all)
 #ifndef AGK_CK

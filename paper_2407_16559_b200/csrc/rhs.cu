@@ -434,15 +434,14 @@ void rhs_make_plan(int64_t m, int rf, RhsPlan* p) {
   // M = 2^20, R = 16: the per-group intermediate then streams through HBM, but the launches and
   // the accumulator round trips of smaller groups cost more), capped at 1 GiB of intermediate.
   int g = (int)((1ll << 30) / (16 * P));
-  if (const char* env = getenv("AGK_RANK_GROUP")) g = atoi(env);
+  g = knob("AGK_RANK_GROUP", g);
   if (g < 1) g = 1;
   if (g > rf) g = rf;
-  const char* fe0 = getenv("AGK_FAST");
-  if (L == 21 && !(fe0 && atoi(fe0) == 0) && g > 16) g = 16;  // warp path: <= 16 rank slots
+  const bool fast = L == 21 && knob("AGK_FAST", 1) != 0;
+  if (fast && g > 16) g = 16;  // warp path: <= 16 rank slots
   p->gsize = g;
   const int ngroups = (rf + g - 1) / g;
-  const char* fe = getenv("AGK_FAST");
-  p->fast = (L == 21) && !(fe && atoi(fe) == 0);
+  p->fast = fast;
   p->launches = p->small ? 1 : 2 * ngroups + 1 + (p->fast ? 2 : 0);  // fast: + transpose, dvec
   p->nsm = 148;
   p->dense = 0;
@@ -473,8 +472,15 @@ static void mark(Marks* mk, int cls, cudaStream_t s) {
 }
 static void mark_cb(void* mk, int cls, cudaStream_t s) { mark(static_cast<Marks*>(mk), cls, s); }
 
+#ifdef AGK_EXPERIMENTS
+int knob(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+#endif
+
 bool pdl_enabled() {
-  static const bool on = !(getenv("AGK_PDL") && atoi(getenv("AGK_PDL")) == 0);
+  static const bool on = knob("AGK_PDL", 1) != 0;
   return on;
 }
 int pdl_mask() {
@@ -482,7 +488,7 @@ int pdl_mask() {
   // pass and the RK-trial chain, and for the four-step path (P = 2^13, and the mid sizes, whose
   // kernels trigger their dependents at their end: -0.5 us at configs 2 and 3; triggered at entry
   // the early-placed dependent grid was slower); off for the column -> row passes
-  static const int m = getenv("AGK_PDLMASK") ? atoi(getenv("AGK_PDLMASK")) : (2 | 8 | 16 | 32 | 64);
+  static const int m = knob("AGK_PDLMASK", 2 | 8 | 16 | 32 | 64);
   return m;
 }
 
@@ -516,11 +522,11 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
 #define AGK_L21_VARIANTS(X) \
   X(0, 16, 16, 8, 0) X(1, 16, 16, 4, 0) X(2, 8, 16, 8, 0) X(6, 16, 16, 8, 1) X(7, 16, 16, 4, 1)
 
+#ifdef AGK_EXPERIMENTS
 static int l21_variant() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("AGK_VARIANT");
-    v = e ? atoi(e) : 0;
+    v = knob("AGK_VARIANT", 0);
   }
   return v;
 }
@@ -532,14 +538,16 @@ static int l21_variant() {
 static int mid_variant() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("AGK_MVAR");
-    v = e ? atoi(e) : 0;
+    v = knob("AGK_MVAR", 0);
   }
   return v;
 }
 
+#endif
+
 template <int L>
 static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
+#ifdef AGK_EXPERIMENTS
   if constexpr (L >= 16 && L <= 20) {
     switch (mid_variant()) {
 #define AGK_M(id, LL, e1, e2, c) \
@@ -558,6 +566,7 @@ static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStre
       default: break;
     }
   }
+#endif
   return launch_four_step_cf<Cfg<L>>(p, a, s, mk);
 }
 
@@ -622,6 +631,7 @@ template <int L>
 static cudaError_t smem_four_step() {
   cudaError_t e = smem_four_step_cf<Cfg<L>>();
   if (e != cudaSuccess) return e;
+#ifdef AGK_EXPERIMENTS
   if constexpr (L == 21) {
 #define AGK_X(id, e1, e2, c, rm) \
   if ((e = smem_four_step_cf<Cfg<21, e1, e2, c, rm>>()) != cudaSuccess) return e;
@@ -634,6 +644,7 @@ static cudaError_t smem_four_step() {
     AGK_MID_VARIANTS(AGK_M, L)
 #undef AGK_M
   }
+#endif
   return e;
 }
 

@@ -47,7 +47,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void tl_mark(const RhsArgs& a, int k, int what) {
-  if ((a.dbg & 512) && threadIdx.x == 0) {
+  if (AGK_XDBG(a, 512) && threadIdx.x == 0) {
     const unsigned long long t = gtimer();
     if (what < 2) atomicMin(&g_timeline[k][what], t);
     else atomicMax(&g_timeline[k][what], t);
@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
   // a quarter of the tile (8 lines per thread), fully unrolled: placed between pieces of step A so
   // the LSU work interleaves with the fp64 work of the transform
   auto store_quarter = [&](int item, int qtr) {
+    if (item < it0 || AGK_XDBG(a, 2)) return;
     const int o = item / gcount, g = item % gcount;
-    if (a.dbg & 2) return;
     double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
 #pragma unroll
     for (int it = 8 * qtr; it < 8 * qtr + 8; ++it) {
@@ -182,18 +182,17 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     if (item + 1 < it1) prefetch(item + 1);
     // L2 bulk prefetch of the item after next: opt-in (AGK_DBG & 32768) since the tile store is
     // interleaved with step A (measured 1.5-2 us faster without; the row pass keeps its prefetch)
-    if (item + a.pfd + 1 < it1 && lane == 0 && (a.dbg & 32768)) {
+    if (item + a.pfd + 1 < it1 && lane == 0 && AGK_XDBG(a, 32768)) {
       const int o2 = (item + a.pfd + 1) / gcount, ub2 = g0 + (item + a.pfd + 1) % gcount;
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
       // the previous item's tile goes out while step A runs (one instruction stream, so the
-      // stores interleave with the transform); the first item stores its own (not yet written)
-      // tile to its own destination, which its real store overwrites later in program order
-      const int sti = item == it0 ? item : item - 1;
+      // stores interleave with the transform); the first item has no previous tile (sti < it0)
+      const int sti = item - 1;
       if constexpr (SV == 0) {
-        if (!(a.dbg & 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
-        if (!(a.dbg & 2)) store_tile(sti);
+        if (!AGK_XDBG(a, 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
+        if (sti >= it0 && !AGK_XDBG(a, 2)) store_tile(sti);
       } else {
         // step A in pieces with a quarter of the tile store after each
         double2 ea[16], ob[16];
@@ -216,11 +215,11 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
         store_quarter(sti, 3);
       }
       __syncthreads();  // every warp has read the tile: it is free for the exchanges
-      if (!(a.dbg & 8)) warp_fft1024_tb<-1>(v, T, w, lane);
+      if (!AGK_XDBG(a, 8)) warp_fft1024_tb<-1>(v, T, w, lane);
     }
     // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
     __syncwarp();
-    if (!(a.dbg & 2048)) {
+    if (!AGK_XDBG(a, 2048)) {
       // four chains t_{j+4m} = (base W_P^{32 n2 j}) (W_P^{128 n2})^m: 5 shared loads instead
       // of 32 on the critical path, at most 7 roundings per factor
       double2 t[4];
@@ -258,7 +257,7 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
       a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
     }
   }
-  if (it0 < it1 && !(a.dbg & 2)) store_tile(it1 - 1);
+  if (it0 < it1 && !AGK_XDBG(a, 2)) store_tile(it1 - 1);
   tl_mark(a, 1, 2);
 }
 
@@ -329,7 +328,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     }
     for (int g = 0; g < gcount; ++g) {
       const double wq = 0.25 * a.uniq_weight[g0 + g];
-      if (lane == 0 && !(a.dbg & 128)) {
+      if (lane == 0 && !AGK_XDBG(a, 128)) {
         // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
         // L2, so the register loads of the next items hit L2
         int gn = g + a.pfd, k1n = k1;
@@ -342,17 +341,17 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           prefetch_l2(a.y + (int64_t)gn * kW_YP + (int64_t)rown * kW_YS + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
-      if (!(a.dbg & 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
+      if (!AGK_XDBG(a, 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
-      if (g + 1 < gcount && !(a.dbg & 64)) {
+      if (g + 1 < gcount && !AGK_XDBG(a, 64)) {
         const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * kW_YP;
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       }
       bar_sync(bar, 128);
-      if (!(a.dbg & 32))
+      if (!AGK_XDBG(a, 32))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int qp = ht + 128 * j;
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(256, 2) k_dvec(RhsArgs a) {
   extern __shared__ double dsm[];  // 4 rf moment totals, 2 r gains, r + 2 scalars
   tl_mark(a, 3, 0);
   tl_mark(a, 3, 1);
-  if (!(a.skip && *a.skip) && !(a.dbg & 256)) {
+  if (!(a.skip && *a.skip) && !AGK_XDBG(a, 256)) {
     const double* __restrict__ n = a.n.get();
     RhsArgs b = a;
     b.flags = a.flags & ~T_BIRTH;
@@ -606,9 +605,8 @@ cudaError_t rhs_w_set_smem_limits() {
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
   RhsArgs a = a0;
-  if (const char* e = getenv("AGK_DBG")) a.dbg = atoi(e);  // experiment switches (tools/ab.sh)
-  a.pfd = 1;                                                 // L2 prefetch distance (items)
-  if (const char* e = getenv("AGK_PFD")) a.pfd = atoi(e);
+  a.dbg = knob("AGK_DBG", 0);  // experiment switches (tools/ab.sh): AGK_EXPERIMENTS builds only
+  a.pfd = knob("AGK_PFD", 1);  // L2 prefetch distance (items)
   const int nsm = p.nsm > 0 ? p.nsm : 148;
   const bool pdl = !mark && pdl_enabled();
   AGK_CK(launch_k(k_transpose_n, (kW_H / 64) * (kW_N2 / 64), 256, 0, s, pdl && (pdl_mask() & 1), a));
@@ -623,7 +621,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
     const int cgrid = items < nsm ? items : nsm;
-    static const int stv = getenv("AGK_STV") ? atoi(getenv("AGK_STV")) : 1;  // 1: measured -3.5 us
+    static const int stv = knob("AGK_STV", 1);  // 1: measured -3.5 us
     if (stv == 1) {
       AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     } else {
@@ -652,7 +650,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     }
     if (mark) mark(mk, K_DVEC, s);
   }
-  static const bool civ4 = getenv("AGK_CIV") && atoi(getenv("AGK_CIV")) == 4;
+  static const bool civ4 = knob("AGK_CIV", 8) == 4;
   if (civ4) {
     AGK_CK(launch_k(k_colinvw<4>, kW_N2 / 8, 128, smem_colinvw4(), s, pdl, a));
   } else {

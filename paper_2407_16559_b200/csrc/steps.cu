@@ -328,9 +328,11 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {      
 __device__ __forceinline__ double inf_d() { return __longlong_as_double(0x7ff0000000000000LL); }
 __device__ __forceinline__ double nan_d() { return __longlong_as_double(0x7ff8000000000000LL); }
 
+// Records go to a device ring; the controller pauses the WHILE loop when the ring is full so
+// the host can drain it (agk_run), hence the slot is never one the host has not copied yet.
 __device__ void push_record(DevCtl* c, double tau, double err) {
-  if (c->rec_buf && c->nrec < c->rec_cap) {
-    agk_record& r = c->rec_buf[c->nrec];
+  if (c->rec_buf && c->nrec - c->rec_drained < c->rec_cap) {
+    agk_record& r = c->rec_buf[c->nrec % c->rec_cap];
     r.t = c->t;
     r.tau = tau;
     r.density = c->mom[0];
@@ -341,6 +343,7 @@ __device__ void push_record(DevCtl* c, double tau, double err) {
     r.rejects = c->rejects_total;
   }
   c->nrec += 1;
+  c->last_rec_t = c->t;
 }
 
 __device__ void ctl_abort(DevCtl* c, int status, double tau_used) {
@@ -388,6 +391,14 @@ __device__ void take_snapshots(DevCtl* c) {
 __global__ void k_prologue(DevCtl* c, const double* mom_part, int nmom, const double* rmax, int nrmax,
                            cudaGraphConditionalHandle h) {
   if (threadIdx.x != 0) return;
+  c->snap_from = c->snap_to = 0;
+  if (c->resume) {  // continuing a run paused to drain the record ring: the loop state stands
+    c->resume = 0;
+    c->paused = 0;
+    cudaGraphSetConditional(h, c->done ? 0u : 1u);
+    return;
+  }
+  c->paused = 0;
   double s[3] = {0.0, 0.0, 0.0};
   for (int b = 0; b < nmom; ++b)
     for (int q = 0; q < 3; ++q) s[q] += mom_part[b * 3 + q];
@@ -419,6 +430,7 @@ __global__ void k_prologue(DevCtl* c, const double* mom_part, int nmom, const do
     }
     c->proposal = proposal;
     begin_step(c);
+    if (!c->done && c->rec_buf && c->nrec - c->rec_drained >= c->rec_cap) c->paused = 1;
   } else {
     c->tau = c->tau_try;
     c->step_rejects = 0;
@@ -428,7 +440,7 @@ __global__ void k_prologue(DevCtl* c, const double* mom_part, int nmom, const do
     c->tau_next = 0.0;
     if (c->mode == AGK_ADAPTIVE && c->tau < c->tau_min) ctl_abort(c, AGK_STEP_TAU_UNDERFLOW, c->tau);
   }
-  cudaGraphSetConditional(h, c->done ? 0u : 1u);
+  cudaGraphSetConditional(h, (c->done || c->paused) ? 0u : 1u);
 }
 
 __global__ void __launch_bounds__(32) k_controller(DevCtl* c, const double* part, int nblk,
@@ -531,9 +543,11 @@ __global__ void __launch_bounds__(32) k_controller(DevCtl* c, const double* part
       }
       take_snapshots(c);
       begin_step(c);
+      // the ring is full: leave the WHILE loop (not done) so the host drains it and resumes
+      if (!c->done && c->rec_buf && c->nrec - c->rec_drained >= c->rec_cap) c->paused = 1;
     }
   }
-  cudaGraphSetConditional(h, c->done ? 0u : 1u);
+  cudaGraphSetConditional(h, (c->done || c->paused) ? 0u : 1u);
 }
 
 // Deep copies of the accepted state for the snapshot times the controller just reached.

@@ -34,8 +34,11 @@ struct DevCtl {
   const double* snap_times;
   double* snap_buf;
   double record_interval;
-  agk_record* rec_buf;
+  agk_record* rec_buf;   // device ring of rec_cap records (drained by the host between segments)
   int64_t rec_cap;
+  long long rec_drained; // records the host has copied out of the ring
+  int resume;            // 1: relaunch after a drain pause (the prologue keeps the loop state)
+  int paused;            // set by the controller when the ring is full: WHILE exits, not done
   int store_n5, has_model;
   // trial / step state
   int cur, k1_valid;
@@ -47,6 +50,7 @@ struct DevCtl {
   double abort_t, abort_tau;
   int snap_idx, snap_from, snap_to;
   long long nrec;
+  double last_rec_t;     // t of the last record pushed (closing-record rule, simulator.cpp:219-222)
   double next_record_t;
   double mom[3];
 };

@@ -126,6 +126,68 @@ int main() {
     expect(a.rejects == b.rejects && rel_max_diff(b.state, a.state) <= 1e-10, "RhsFn seam: reference steppers on the device RHS",
            rel_max_diff(b.state, a.state), 1e-10);
   }
+  // 5. one workspace, two models (rhs.hpp:89-90: the model is a per-call argument): the
+  //    workspace rebinds on a model change and the eval counter carries over
+  {
+    const std::size_t m = 3000;
+    const ModelSpec a = make_model(ModelVariant::aggregation, specs[1], m);
+    const ModelSpec b = make_model(ModelVariant::aggregation_shattering, specs[2], m);
+    RhsWorkspace cpu_ws;
+    gpu::GpuWorkspace gws;
+    std::vector<double> n(m), want(m), got(m);
+    for (double& x : n) x = uni(rng);
+    double worst2 = 0.0;
+    for (const ModelSpec* model : {&a, &b, &a, &b}) {
+      eval_rhs(*model, n, cpu_ws, want);
+      gpu::eval_rhs(*model, n, gws, got);
+      worst2 = std::max(worst2, rel_max_diff(got, want));
+    }
+    expect(worst2 <= 1e-11, "two models through one workspace: eval_rhs follows the model argument", worst2, 1e-11);
+    expect(gws.evals() == 4 && cpu_ws.evals() == 4, "two models: eval counter carries over rebinding",
+           (double)gws.evals(), 4.0);
+    std::vector<double> wt(m), gt(m);
+    death_term(b.kernel, n, cpu_ws, wt);
+    gpu::death_term(b.kernel, n, gws, gt);
+    const double d1 = rel_max_diff(gt, wt);
+    birth_term(a.kernel, n, cpu_ws, wt);
+    gpu::birth_term(a.kernel, n, gws, gt);
+    const double d2 = rel_max_diff(gt, wt);
+    shattering_terms(b.kernel, n, 0.02, cpu_ws, wt);
+    gpu::shattering_terms(b.kernel, n, 0.02, gws, gt);
+    const double d3 = rel_max_diff(gt, wt);
+    expect(std::max({d1, d2, d3}) <= 1e-11, "two models: term functions follow the kernel argument",
+           std::max({d1, d2, d3}), 1e-11);
+    const double eb_want = euler_stability_bound(b.kernel, n, 0.25), eb_got = gpu::euler_stability_bound(b.kernel, n, 0.25);
+    expect(std::abs(eb_got - eb_want) <= 1e-12 * eb_want, "euler_stability_bound with the reference signature",
+           eb_got, eb_want);
+  }
+
+  // 6. run with more records than the device ring holds (1 << 16): every record comes back
+  //    (simulator.cpp:130-145, 209-222)
+  {
+    SimulationConfig cfg;
+    cfg.model = make_model(ModelVariant::aggregation, specs[0], 64);
+    cfg.control.stepper = StepperKind::rk2;
+    cfg.control.mode = StepMode::fixed;
+    cfg.control.tau = 1e-3;
+    cfg.t_end = 150.0;
+    cfg.snapshot_times = {75.0};
+    cfg.record = RecordMode::every_step;
+    const RunReport want = run(cfg);
+    const RunReport got = gpu::run(cfg);
+    bool same = got.records.size() == want.records.size();
+    double dt = 0.0, dd = 0.0;
+    for (std::size_t q = 0; same && q < want.records.size(); ++q) {
+      same = got.records[q].rhs_evals == want.records[q].rhs_evals && got.records[q].rejects == want.records[q].rejects;
+      dt = std::max(dt, std::abs(got.records[q].t - want.records[q].t) / std::max(1.0, want.records[q].t));
+      dd = std::max(dd, std::abs(got.records[q].density - want.records[q].density) / want.records[q].density);
+    }
+    expect(want.records.size() > 100000 && same, "run: > 65536 records, counts identical record by record",
+           (double)got.records.size(), (double)want.records.size());
+    expect(dt <= 1e-12 && dd <= 1e-9, "run: long record stream t and density", dt, dd);
+    expect(got.total_accepted == want.total_accepted && got.snapshots.size() == 1, "run: long run counters",
+           (double)got.total_accepted, (double)want.total_accepted);
+  }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;
 }

@@ -1,0 +1,123 @@
+"""Full-integration parity goldens from the REFERENCE itself (oracle/_ref), TEST INFRASTRUCTURE.
+
+SURVEY §8d's parity plan (VERDICT r1 "Next round" item 1): full-shape prefixes and reduced-M full
+horizons of BASELINE configs 1, 2, 3 and 5, run by the reference's own run() (simulator.cpp:
+112-229, compiled from /root/reference sources by oracle/Makefile), plus the same case run by a
+second, equally valid CPU build (the C restatement with FMA contraction, or with a 2x-padded FFT)
+whose distance from the reference is the CPU-vs-CPU noise floor reported beside every GPU number.
+
+Run here (where /root/reference exists), one process per case (they are single-threaded):
+
+    python tests/golden/make_parity_runs.py --list
+    python tests/golden/make_parity_runs.py CASE [--floor port_fma]
+
+Writes tests/golden/parity/CASE__ref.npz and CASE__floor.npz. The state is stored compactly: the head of the final state
+up to the last index with n_s > 1e-13 max n (everything that can move the normwise or element-wise
+bars) and the max |n_s| of the tail beyond it.
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import oracle as O  # noqa: E402
+
+OUT = os.path.join(HERE, "parity")
+HEAD_REL = 1e-13
+
+# BASELINE.json configs: (kernel, variant, sources, lambda, initial, tol)
+CONFIG = {
+    1: ("constant", O.AGGREGATION, [], 0.0, "mono", 1e-6),
+    2: ("brownian2", O.SOURCES, [(1, 1.0)], 0.0, "zero", 1e-6),
+    3: ("brownian0.9", O.SHATTERING, [], 0.01, "mono", 1e-8),
+    5: ("brownian2", O.SOURCES, [(1, 1.0)], 0.0, "zero", 1e-6),
+}
+STEPPERS = {"rk2": O.RK2, "rk4": O.RK4, "rkf45": O.RKF45}
+
+# name -> (config, m, stepper, t_end)
+CASES = {}
+for s in STEPPERS:
+    CASES[f"c1_full_{s}"] = (1, 4096, s, 100.0)                 # config 1, full shape and horizon
+    CASES[f"c2_m4096_{s}"] = (2, 4096, s, 1e4)                  # config 2 full horizon, reduced M
+    CASES[f"c5_m4096_{s}"] = (5, 4096, s, 1e5)                  # config 5 full horizon, reduced M
+    CASES[f"c5_full_t2_{s}"] = (5, 1 << 20, s, 2.0)             # config 5 full shape, prefix
+CASES["c3_m2048_rkf45"] = (3, 2048, "rkf45", 5000.0)            # config 3 full horizon, reduced M
+CASES["c3_full_t1_rkf45"] = (3, 1 << 17, "rkf45", 1.0)          # config 3 full shape, prefix
+CASES["c2_full_rkf45"] = (2, 1 << 16, "rkf45", 1e4)             # config 2 full shape and horizon
+
+
+def model_for(cfg, m):
+    kind, var, srcs, lam, init, tol = CONFIG[cfg]
+    if kind == "constant":
+        u, v = O.constant_factors(m)
+    elif kind == "brownian2":
+        u, v = O.brownian_plus2_factors(m)
+    else:
+        u, v = O.brownian_factors(m, float(kind[len("brownian"):]))
+    n0 = np.zeros(m)
+    if init == "mono":
+        n0[0] = 1.0
+    return O.Model(u, v, var, list(srcs), lam), n0, tol
+
+
+def case_inputs(name):
+    cfg, m, st, t_end = CASES[name]
+    md, n0, tol = model_for(cfg, m)
+    ctl = O.Control(stepper=STEPPERS[st], mode=O.ADAPTIVE, tol=tol)
+    return md, n0, ctl, t_end
+
+
+def summarize(r):
+    x = np.asarray(r["final_state"])
+    k = np.arange(1, x.size + 1, dtype=np.float64)
+    mx = float(np.max(np.abs(x))) if x.size else 0.0
+    sig = np.nonzero(np.abs(x) > HEAD_REL * mx)[0]
+    head = int(sig[-1]) + 1 if sig.size else 0
+    return dict(termination=int(r["termination"]), final_t=float(r["final_t"]),
+                accepted=int(r["total_accepted"]), rejects=int(r["total_rejects"]),
+                rhs_evals=int(r["total_rhs_evals"]), N=float(x.sum()), M1=float(np.dot(k, x)),
+                M2=float(np.dot(k * k, x)), n1=float(x[0]), maxn=mx,
+                head=x[:head].copy(), tail_maxabs=float(np.max(np.abs(x[head:]))) if head < x.size else 0.0)
+
+
+def run_one(which, name):
+    md, n0, ctl, t_end = case_inputs(name)
+    t0 = time.time()
+    r = O.Oracle(which).run(md, n0, ctl, t_end, record=O.RECORD_NONE)
+    s = summarize(r)
+    s["wall_s"] = time.time() - t0
+    return s
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("case", nargs="?")
+    ap.add_argument("--list", action="store_true")
+    ap.add_argument("--floor", default="port_fma", help="second CPU build for the noise floor ('' = none)")
+    ap.add_argument("--which", default="both", choices=["both", "ref", "floor"])
+    a = ap.parse_args()
+    if a.list or not a.case:
+        print("\n".join(CASES))
+        return
+    os.makedirs(OUT, exist_ok=True)
+    cfg, m, st, t_end = CASES[a.case]
+    legs = []
+    if a.which in ("both", "ref"):
+        legs.append(("ref", "reference"))
+    if a.which in ("both", "floor") and a.floor:
+        legs.append(("floor", a.floor))
+    for key, which in legs:
+        s = run_one(which, a.case)
+        out = dict(config=np.array(cfg), m=np.array(m), stepper=np.array(st), t_end=np.array(t_end),
+                   build=np.array(which))
+        out.update({k: np.asarray(v) for k, v in s.items()})
+        print(a.case, key, which, {k: v for k, v in s.items() if k != "head"}, flush=True)
+        np.savez_compressed(os.path.join(OUT, f"{a.case}__{key}.npz"), **out)
+
+if __name__ == "__main__":
+    main()

@@ -195,7 +195,7 @@ def test_records_match_oracle(agk, oracle_port):
     n0[0] = 1.0
     ctl = dict(stepper=O.RK4, tol=1e-8)
     g = agk.run(ws, agk.SimulationConfig(agk.StepControl(**ctl), 3.0, n0, snapshot_times=[0.0, 0.3777, 1.5, 3.0],
-                                         record=agk.RECORD_EVERY_STEP, records_capacity=10000))
+                                         record=agk.RECORD_EVERY_STEP))
     w = oracle_port.run(om, n0, O.Control(**ctl), 3.0, snapshot_times=[0.0, 0.3777, 1.5, 3.0],
                         record=O.RECORD_EVERY_STEP, records_capacity=10000)
     assert g.num_records == w["num_records"]
@@ -284,7 +284,7 @@ def test_config5_reduced_m(agk, oracle_port, stepper):
     om, ws = build(agk, "brownian2", 4096, variant=O.SOURCES, sources=[(1, 1.0)])
     n0 = np.zeros(4096)
     g = agk.run(ws, agk.SimulationConfig(agk.StepControl(stepper=stepper, tol=1e-6), 50.0, n0,
-                                         record=agk.RECORD_EVERY_STEP, records_capacity=100000))
+                                         record=agk.RECORD_EVERY_STEP))
     w, f = oracle_pair(om, n0, dict(stepper=stepper, tol=1e-6), 50.0, record=O.RECORD_EVERY_STEP,
                        records_capacity=100000)
     check_lockstep(g, w, f)
@@ -296,8 +296,30 @@ def test_config3_reduced_m(agk, oracle_port):
     om, ws = build(agk, "brownian", 2048, 0.9, O.SHATTERING, lam=0.01)
     n0 = np.zeros(2048)
     n0[0] = 1.0
-    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(tol=1e-8), 20.0, n0, record=agk.RECORD_EVERY_STEP,
-                                         records_capacity=100000))
+    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(tol=1e-8), 20.0, n0, record=agk.RECORD_EVERY_STEP))
     w, f = oracle_pair(om, n0, dict(tol=1e-8), 20.0, record=O.RECORD_EVERY_STEP, records_capacity=100000)
     check_lockstep(g, w, f)
     check_run(g, w, f)
+
+
+def test_record_stream_past_ring(agk, oracle_port):
+    """More records than the device ring holds (1 << 16): the run pauses to drain the ring and
+    every record comes back, identical in count and order to the reference's RunReport
+    (simulator.cpp:130-145, 209-222). Fixed RK2 steps: the same decisions on both sides."""
+    om, ws = build(agk, "constant", 64)
+    n0 = np.zeros(64)
+    n0[0] = 1.0
+    ctl = dict(stepper=O.RK2, mode=O.FIXED, tau=1e-3)
+    g = agk.run(ws, agk.SimulationConfig(agk.StepControl(**ctl), 150.0, n0, snapshot_times=[75.0],
+                                         record=agk.RECORD_EVERY_STEP))
+    w = oracle_port.run(om, n0, O.Control(**ctl), 150.0, snapshot_times=[75.0], record=O.RECORD_EVERY_STEP,
+                        records_capacity=200000)
+    assert g.num_records == w["num_records"] == len(g.records) > 140000
+    assert [r["rhs_evals"] for r in g.records] == [r["rhs_evals"] for r in w["records"]]
+    gt = np.array([r["t"] for r in g.records])
+    wt = np.array([r["t"] for r in w["records"]])
+    assert np.max(np.abs(gt - wt) / np.maximum(wt, 1.0)) <= 1e-12
+    gd = np.array([r["density"] for r in g.records])
+    wd = np.array([r["density"] for r in w["records"]])
+    assert np.max(np.abs(gd / wd - 1.0)) <= 1e-9
+    assert len(g.snapshots) == 1 and g.snapshots[0][0] == 75.0

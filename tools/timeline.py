@@ -2,6 +2,9 @@
 per kernel class the first CTA's arrival, the first CTA's start of work after its
 programmatic-dependency wait, and the last CTA's exit, in us from the first arrival."""
 import ctypes, os, sys
+# AGK_* knobs are read only by the experiments build (make -C paper_2407_16559_b200 exp)
+os.environ.setdefault("AGK_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                              "paper_2407_16559_b200", "libagk_b200_exp.so"))
 os.environ["AGK_DBG"] = str(int(os.environ.get("AGK_DBG", "0")) | 512)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch

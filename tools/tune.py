@@ -19,7 +19,9 @@ print(json.dumps(dict(ms=ms, cls=cls, plan=plan, chk=float(od.abs().sum()))))
 variants = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0"]
 groups = sys.argv[2].split(",") if len(sys.argv) > 2 else ["1"]
 for v, g in itertools.product(variants, groups):
-    env = dict(os.environ, AGK_VARIANT=v, AGK_RANK_GROUP=g)
+    # AGK_* knobs are read only by the experiments build (make -C paper_2407_16559_b200 exp)
+    env = dict(os.environ, AGK_VARIANT=v, AGK_RANK_GROUP=g,
+               AGK_LIB=os.path.join(ROOT, "paper_2407_16559_b200", "libagk_b200_exp.so"))
     r = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True, timeout=300)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-500:]
     print(f"variant={v} group={g}: {line}", flush=True)
