@@ -106,9 +106,11 @@ enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANS
 #ifdef AGK_EXPERIMENTS
 int knob(const char* name, int dflt);
 #define AGK_XDBG(a, bits) (((a).dbg & (bits)) != 0)
+#define AGK_PFDIST(a) ((a).pfd)
 #else
 inline int knob(const char*, int dflt) { return dflt; }
 #define AGK_XDBG(a, bits) false
+#define AGK_PFDIST(a) 1  // L2 prefetch distance of the row pass (items), measured best
 #endif
 bool pdl_enabled();
 int pdl_mask();  // AGK_PDLMASK experiment bits (default all)

@@ -131,11 +131,9 @@ __device__ __forceinline__ void finalize_scalars_cta(const RhsArgs& a, const dou
 
 // Epilogue for output index jo >= 1: S = birth - death [+ shattering loss] [+ sources], with the
 // death row sum sum_a U_sa w_a given (ascending a, as rhs.cpp:24-46 accumulates it)
-__device__ __forceinline__ double epilogue_rs(const RhsArgs& a, const double* __restrict__ n, int64_t jo,
-                                              double birth, double rowsum) {
+__device__ __forceinline__ double epilogue_rsn(const RhsArgs& a, double nn, int64_t jo, double birth, double rowsum) {
   double res = (a.flags & T_BIRTH) ? birth : 0.0;
   if (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) {
-    const double nn = n[jo];
     if (a.flags & T_DEATH) res = res - nn * rowsum;
     if (a.flags & T_DEATH_POS) res = nn * rowsum;
     if (a.flags & T_SHATTER) res = res + (-a.lambda * nn) * rowsum;
@@ -145,6 +143,10 @@ __device__ __forceinline__ double epilogue_rs(const RhsArgs& a, const double* __
       if (a.src_k[q] - 1 == jo) res += a.src_rate[q];
   }
   return res;
+}
+__device__ __forceinline__ double epilogue_rs(const RhsArgs& a, const double* __restrict__ n, int64_t jo,
+                                              double birth, double rowsum) {
+  return epilogue_rsn(a, (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) ? n[jo] : 0.0, jo, birth, rowsum);
 }
 __device__ __forceinline__ double epilogue(const RhsArgs& a, const double* __restrict__ n,
                                            int64_t jo, double birth) {

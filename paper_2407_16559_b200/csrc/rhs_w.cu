@@ -182,8 +182,8 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
     if (item + 1 < it1) prefetch(item + 1);
     // L2 bulk prefetch of the item after next: opt-in (AGK_DBG & 32768) since the tile store is
     // interleaved with step A (measured 1.5-2 us faster without; the row pass keeps its prefetch)
-    if (item + a.pfd + 1 < it1 && lane == 0 && AGK_XDBG(a, 32768)) {
-      const int o2 = (item + a.pfd + 1) / gcount, ub2 = g0 + (item + a.pfd + 1) % gcount;
+    if (item + AGK_PFDIST(a) + 1 < it1 && lane == 0 && AGK_XDBG(a, 32768)) {
+      const int o2 = (item + AGK_PFDIST(a) + 1) / gcount, ub2 = g0 + (item + AGK_PFDIST(a) + 1) % gcount;
       prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
     }
     {
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       if (lane == 0 && !AGK_XDBG(a, 128)) {
         // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
         // L2, so the register loads of the next items hit L2
-        int gn = g + a.pfd, k1n = k1;
+        int gn = g + AGK_PFDIST(a), k1n = k1;
         if (gn >= gcount) {
           gn -= gcount;
           k1n += 2 * gridDim.x;
