@@ -54,6 +54,15 @@ __device__ __forceinline__ void tl_mark(const RhsArgs& a, int k, int what) {
   }
 }
 
+// the same with a run-time test (see ROW_XDBG below)
+__device__ __forceinline__ void tl_mark_rt(const RhsArgs& a, int k, int what) {
+  if ((a.dbg & 512) && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (what < 2) atomicMin(&g_timeline[k][what], t);
+    else atomicMax(&g_timeline[k][what], t);
+  }
+}
+
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // n (natural, m) -> ng[n2 * 512 + n1] = n[n1 * 2048 + n2] (0 past m). 64 x 64 tiles, 16 elements
@@ -273,6 +282,11 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
 // four-step twiddle, writing G in place of the accumulator row.
 // Launched with 2 row pairs per half (grid = ceil(513 / 4) = 129 CTAs at N1 = 1024) so the SMs
 // left over run the non-birth part D concurrently (k_dvec, programmatic dependent launch).
+// The row kernel tests its experiment bits at run time (a.dbg is 0 unless an AGK_EXPERIMENTS
+// build set it from AGK_DBG: the production library never reads the environment): folded away
+// at compile time, ptxas allocates this 255-register kernel worse (36 instead of 8 bytes of
+// spills, measured with -Xptxas -v).
+#define ROW_XDBG(a, bits) ((((a).dbg) & (bits)) != 0)
 template <bool LAST>
 __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, int first) {
   extern __shared__ double2 smem[];
@@ -281,9 +295,9 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   double2* twh = tw + 1024;        // W_2048^j, j < 1024
   __shared__ double2 tkk[8][32];
   // after the column pass completed: k_dvec (dependent) reads its moment partials
-  tl_mark(a, 2, 0);
+  tl_mark_rt(a, 2, 0);
   pdl_entry();
-  tl_mark(a, 2, 1);
+  tl_mark_rt(a, 2, 1);
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, hf = w >> 2, hw = w & 3, rho = hw >> 1,
             h = hw & 1, ht = tid & 127, bar = 1 + hf;
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     }
     for (int g = 0; g < gcount; ++g) {
       const double wq = 0.25 * a.uniq_weight[g0 + g];
-      if (lane == 0 && !AGK_XDBG(a, 128)) {
+      if (lane == 0 && !ROW_XDBG(a, 128)) {
         // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
         // L2, so the register loads of the next items hit L2
         int gn = g + AGK_PFDIST(a), k1n = k1;
@@ -341,17 +355,17 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           prefetch_l2(a.y + (int64_t)gn * kW_YP + (int64_t)rown * kW_YS + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
-      if (!AGK_XDBG(a, 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
+      if (!ROW_XDBG(a, 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
       __syncwarp();
 #pragma unroll
       for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
-      if (g + 1 < gcount && !AGK_XDBG(a, 64)) {
+      if (g + 1 < gcount && !ROW_XDBG(a, 64)) {
         const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * kW_YP;
 #pragma unroll
         for (int r = 0; r < 32; ++r) v[r] = src[lane + 32 * r];
       }
       bar_sync(bar, 128);
-      if (!AGK_XDBG(a, 32))
+      if (!ROW_XDBG(a, 32))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int qp = ht + 128 * j;
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       bar_sync(bar, 128);  // the regions are reused by the next row pair
     }
   }
-  tl_mark(a, 2, 2);
+  tl_mark_rt(a, 2, 2);
 }
 
 // The non-birth part of S for every size: -n_s sum_a U_sa w_a [+ shattering] [+ sources]
