@@ -104,6 +104,31 @@ __device__ __forceinline__ void finalize_scalars(const RhsArgs& a, const double*
 
 // The same, by a whole CTA: each thread finishes its ranks' w_a and gain terms (the loads of
 // all ranks in flight together), then thread 0 sums the gains in rank order. sh: 2 r doubles.
+__device__ __forceinline__ void finalize_scalars_to(const RhsArgs& a, const double* tot, double n0, double* sh,
+                                                    double* scal) {
+  for (int ra = threadIdx.x; ra < a.r; ra += blockDim.x) {
+    const int code = a.rank_map[ra];
+    const bool sw = code >= kSwap;
+    const int ub = sw ? code - kSwap : code;
+    const double A0 = tot[ub * 4 + 0], A1 = tot[ub * 4 + 1];
+    const double B0 = tot[ub * 4 + 2], B1 = tot[ub * 4 + 3];
+    const double su0 = sw ? B0 : A0, su1 = sw ? B1 : A1;
+    const double sv0 = sw ? A0 : B0, sv1 = sw ? A1 : B1;
+    scal[ra] = sv0 + a.v0[ra] * n0;  // w_a = sum_j V_aj n_j
+    sh[2 * ra] = su1 * sv0 + su0 * sv1;
+    sh[2 * ra + 1] = a.u0[ra] * sv1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pair = 0.0, mono = 0.0;
+    for (int ra = 0; ra < a.r; ++ra) {
+      pair += sh[2 * ra];
+      mono += sh[2 * ra + 1];
+    }
+    scal[a.r] = pair;
+    scal[a.r + 1] = mono;
+  }
+}
 __device__ __forceinline__ void finalize_scalars_cta(const RhsArgs& a, const double* tot, double n0, double* sh) {
   for (int ra = threadIdx.x; ra < a.r; ra += blockDim.x) {
     const int code = a.rank_map[ra];
@@ -167,6 +192,36 @@ __device__ __forceinline__ double epilogue(const RhsArgs& a, const double* __res
     for (; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + jo) * a.scalars[ra];
   }
   return epilogue_rs(a, n, jo, birth, rowsum);
+}
+
+// D = the non-birth part of S at output index jo >= 1 (death, shattering loss, sources) from the
+// row sum and n_jo, for term flags `fl` (epilogue_rsn with T_BIRTH cleared, without an RhsArgs copy)
+__device__ __forceinline__ double dvalue(const RhsArgs& a, int fl, double nn, int64_t jo, double rowsum) {
+  double res = 0.0;
+  if (fl & T_DEATH) res = res - nn * rowsum;
+  if (fl & T_DEATH_POS) res = nn * rowsum;
+  if (fl & T_SHATTER) res = res + (-a.lambda * nn) * rowsum;
+  if (fl & T_SOURCES) {
+    for (int q = 0; q < a.nsrc; ++q)
+      if (a.src_k[q] - 1 == jo) res += a.src_rate[q];
+  }
+  return res;
+}
+// D at index 0 (epilogue0 with the scalars w_a, pair, mono in `scal`)
+__device__ __forceinline__ double dvalue0(const RhsArgs& a, int fl, const double* scal, double n0) {
+  double res = 0.0;
+  if (fl & (T_DEATH | T_DEATH_POS)) {
+    double rowsum = 0.0;
+    for (int ra = 0; ra < a.r; ++ra) rowsum += a.ut[(int64_t)ra * a.m] * scal[ra];
+    if (fl & T_DEATH) res = res - n0 * rowsum;
+    if (fl & T_DEATH_POS) res = n0 * rowsum;
+  }
+  if (fl & T_SHATTER) res = res + (0.5 * a.lambda * scal[a.r] + a.lambda * n0 * scal[a.r + 1]);
+  if (fl & T_SOURCES) {
+    for (int q = 0; q < a.nsrc; ++q)
+      if (a.src_k[q] == 1) res += a.src_rate[q];
+  }
+  return res;
 }
 
 // out[0]: no birth; death; shattering gain at s = 1 (rhs.cpp:208); sources at k = 1.

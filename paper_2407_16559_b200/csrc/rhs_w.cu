@@ -428,78 +428,104 @@ __global__ void __launch_bounds__(256, 2) k_dvec(RhsArgs a) {
   tl_mark(a, 3, 1);
   if (!(a.skip && *a.skip) && !AGK_XDBG(a, 256)) {
     const double* __restrict__ n = a.n.get();
-    RhsArgs b = a;
-    b.flags = a.flags & ~T_BIRTH;
-    // w_a and the shattering gains from the column pass' moment partials, reduced by every CTA
-    // in the same fixed order (bitwise identical copies; nothing on the critical path)
-    {
-      double* tot = dsm;
-      double* sh = tot + 4 * a.rf;
-      b.scalars = sh + 2 * a.r;
-      reduce_partials_wide(a, a.nblk_colfwd, tot);
-      __syncthreads();
-      finalize_scalars_cta(b, tot, n[0], sh);
-      __syncthreads();
-      if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < a.r + 2; i += blockDim.x) a.scalars[i] = b.scalars[i];
-    }
+    const int fl = a.flags & ~T_BIRTH;
     const bool rs = (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) != 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if ((a.m & 1) == 0) {
-      // 4 x 2 sizes per thread (16-byte loads of U^T, four independent row-sum chains so the
-      // loads of one rank step are in flight together); each size's sum runs in rank order
-      const int64_t np = a.m / 2;
-      for (int64_t p0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p0 < np; p0 += 4 * stride) {
-        double r[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    const bool even = (a.m & 1) == 0;
+    // Even m: KU x 2 sizes per thread per batch (16-byte loads); the U^T rows of the first RB
+    // ranks and the n pairs of a batch are issued together (they do not depend on w), the first
+    // batch before the scalars are final and each next batch before the current one is stored,
+    // so a batch costs one round trip for r <= RB.
+    constexpr int KU = 2, RB = 4;
+    const int64_t np = a.m / 2;
+    const int64_t pbeg = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double2 nv[KU], u[RB][KU];
+    auto issue = [&](int64_t p0) {
+#pragma unroll
+      for (int k = 0; k < KU; ++k) {
+        const int64_t pk = 2 * (p0 + k * stride < np ? p0 + k * stride : np - 1);  // clamped
+        nv[k] = *reinterpret_cast<const double2*>(n + pk);
+#pragma unroll
+        for (int q = 0; q < RB; ++q)
+          u[q][k] = (rs && q < a.r) ? __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)q * a.m + pk))
+                                     : make_double2(0.0, 0.0);
+      }
+    };
+    // w_a and the shattering gains from the column pass' moment partials, reduced by every CTA
+    // in the same fixed order (bitwise identical copies); the first batch goes out between the
+    // (register-heavy) partial sums and the (latency-bound) finalisation
+    double* tot = dsm;
+    double* sh = tot + 4 * a.rf;
+    double* scal = sh + 2 * a.r;  // w_a, pair gain, monomer gain
+    reduce_partials_wide(a, a.nblk_colfwd, tot);
+    if (even && pbeg < np) issue(pbeg);
+    __syncthreads();
+    finalize_scalars_to(a, tot, n[0], sh, scal);
+    __syncthreads();
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < a.r + 2; i += blockDim.x) a.scalars[i] = scal[i];
+    if (even) {
+      for (int64_t p0 = pbeg; p0 < np; p0 += KU * stride) {
+        double r[KU][2];
+#pragma unroll
+        for (int k = 0; k < KU; ++k) r[k][0] = r[k][1] = 0.0;
         if (rs) {
-          int64_t pk[4];
+          // each size's row sum in rank order (rhs.cpp:24-46): ranks < RB from the batch
+          // registers, the rest RB at a time
 #pragma unroll
-          for (int k = 0; k < 4; ++k) pk[k] = 2 * (p0 + k * stride < np ? p0 + k * stride : np - 1);  // clamped
-          int ra = 0;
-          // four ranks per step: 16 independent 16-byte loads in flight per thread (the kernel runs
-          // on the few SMs the row pass leaves free, so its memory parallelism is per thread)
-          for (; ra + 4 <= a.r; ra += 4) {
-            double2 u[4][4];
+          for (int q = 0; q < RB; ++q) {
+            if (q < a.r) {
+              const double w = scal[q];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                u[q][k] = __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)(ra + q) * a.m + pk[k]));
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const double w = b.scalars[ra + q];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
+              for (int k = 0; k < KU; ++k) {
                 r[k][0] += u[q][k].x * w;
                 r[k][1] += u[q][k].y * w;
               }
             }
           }
-          for (; ra < a.r; ++ra) {
-            const double w = b.scalars[ra];
-            double2 u[4];
+          for (int ra = RB; ra < a.r; ra += RB) {  // (the batch registers are free again)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)ra * a.m + pk[k]));
+            for (int q = 0; q < RB; ++q)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              r[k][0] += u[k].x * w;
-              r[k][1] += u[k].y * w;
+              for (int k = 0; k < KU; ++k) {
+                const int64_t pk = 2 * (p0 + k * stride < np ? p0 + k * stride : np - 1);
+                u[q][k] = ra + q < a.r ? __ldg(reinterpret_cast<const double2*>(a.ut + (int64_t)(ra + q) * a.m + pk))
+                                       : make_double2(0.0, 0.0);
+              }
+#pragma unroll
+            for (int q = 0; q < RB; ++q) {
+              if (ra + q < a.r) {
+                const double w = scal[ra + q];
+#pragma unroll
+                for (int k = 0; k < KU; ++k) {
+                  r[k][0] += u[q][k].x * w;
+                  r[k][1] += u[q][k].y * w;
+                }
+              }
             }
           }
         }
+        double2 nk[KU];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < KU; ++k) nk[k] = nv[k];
+        if (p0 + KU * stride < np) issue(p0 + KU * stride);  // the next batch's loads go out now
+#pragma unroll
+        for (int k = 0; k < KU; ++k) {
           const int64_t p = p0 + k * stride;
           if (p < np) {
             const int64_t s = 2 * p;
-            a.dvec[s] = s == 0 ? epilogue0(b, n) : epilogue_rs(b, n, s, 0.0, r[k][0]);
-            a.dvec[s + 1] = epilogue_rs(b, n, s + 1, 0.0, r[k][1]);
+            a.dvec[s] = s == 0 ? dvalue0(a, fl, scal, nk[k].x) : dvalue(a, fl, nk[k].x, s, r[k][0]);
+            a.dvec[s + 1] = dvalue(a, fl, nk[k].y, s + 1, r[k][1]);
           }
         }
       }
     } else {
-      for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < a.m; s += stride)
-        a.dvec[s] = s == 0 ? epilogue0(b, n) : epilogue(b, n, s, 0.0);
+      for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < a.m; s += stride) {
+        double rowsum = 0.0;
+        if (rs)
+          for (int ra = 0; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * a.m + s) * scal[ra];
+        a.dvec[s] = s == 0 ? dvalue0(a, fl, scal, n[0]) : dvalue(a, fl, n[s], s, rowsum);
+      }
     }
   }
   tl_mark(a, 5, 2);  // D done (before the wait for the row grid)
