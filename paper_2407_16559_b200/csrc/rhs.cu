@@ -173,7 +173,6 @@ struct Cfg {
 
 template <int N1, int E1, int C>
 __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int gcount) {
-  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   using PL = FftPlan<N1, E1>;
   constexpr int T1 = N1 / E1, NT = C * T1, H = E1 / 2;
   constexpr int RG = PL::template smem<kNoPad>();
@@ -181,7 +180,6 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   double2* smtw = smem + C * RG;
   double* stage = reinterpret_cast<double*>(smtw + PL::TWS);  // [2][H][NT]: own elements only
   __shared__ double red[((NT + 31) / 32) * 4];
-  if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, c = tid % C, j = tid / C;
   const int64_t n2 = (int64_t)blockIdx.x * C + c;
   const int64_t N2 = a.n2, m = a.m, P = (int64_t)N1 * N2;
@@ -199,8 +197,14 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
     }
     cp_async_commit();
   };
+  // immutable operands (U, V, tables) first: they overlap the predecessor's tail
   if (gcount > 0) prefetch(g0);
   load_twiddles<N1, E1>(smtw, a.tw_n1);
+  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
+  if (a.skip && *a.skip) {
+    cp_async_wait_all();
+    return;
+  }
   const double* __restrict__ n = a.n.get();
   double nl[H];
 #pragma unroll
@@ -250,12 +254,13 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
 
 template <int N2, int E2, bool STAGE, int MINB>
 __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, int gcount, int first, int last) {
-  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   using PL = FftPlan<N2, E2>;
   constexpr int T2 = N2 / E2, NT = 2 * T2, Q = E2 / 2;
   extern __shared__ double2 smem[];
   double2* smtw = smem + 2 * PL::SMEM;
   double2* stage = smtw + PL::TWS;  // [E2][NT]: this thread's elements of the next rank's row
+  load_twiddles<N2, E2>(smtw, a.tw_n2);  // immutable table: overlaps the predecessor's tail
+  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, team = tid / T2, j = tid % T2;
   const int n1 = a.n1;
@@ -270,15 +275,16 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
       cp_async_commit();
     }
   };
-  if (gcount > 0) prefetch(0);
-  load_twiddles<N2, E2>(smtw, a.tw_n2);
-
-  if (last && blockIdx.x == 0) {
+  if (last && k1 == n1 / 2 + 1) {
+    // the extra CTA of the last launch: w_a and the shattering gains from the column pass'
+    // moment partials, beside the row transforms instead of ahead of one of them
     double* tot = a.scalars + a.r + 2;
-    reduce_partials(a, a.nblk_colfwd, tot);
+    reduce_partials(a, a.nblk_colfwd, tot);  // (register-light: the row kernel's budget is tight)
     __syncthreads();
     if (tid == 0) finalize_scalars(a, tot, a.n.get()[0]);
+    return;
   }
+  if (gcount > 0) prefetch(0);
 
   double2 acc[Q];
 #pragma unroll
@@ -345,14 +351,14 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
 
 template <int N1, int E1, int CP>
 __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
-  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   using PL = FftPlan<N1, E1>;
   constexpr int T1 = N1 / E1;
   constexpr int RG = PL::template smem<kNoPad>();
   extern __shared__ double2 smem[];
   double2* smtw = smem + CP * RG;
+  load_twiddles<N1, E1>(smtw, a.tw_n1);  // immutable table: overlaps the predecessor's tail
+  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   if (a.skip && *a.skip) return;
-  load_twiddles<N1, E1>(smtw, a.tw_n1);
   const int tid = threadIdx.x, c = tid % CP, j = tid / CP;
   const int64_t N2 = a.n2, m = a.m;
   const int64_t col = (int64_t)blockIdx.x * 2 * CP + 2 * c;
@@ -370,15 +376,40 @@ __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
     }
     v[r] = make_double2(ga.x - gb.y, ga.y + gb.x);  // G_a + i G_b: two real outputs at once
   }
+  // the epilogue's other inputs (n, the U rows of up to 4 ranks, w_a) do not depend on the
+  // transform: their loads go out with G's and land while the FFT runs
+  const double* __restrict__ n = a.n.get();
+  const bool rs = (a.flags & (T_DEATH | T_DEATH_POS | T_SHATTER)) != 0;
+  constexpr int NO = E1;  // outputs per thread: 2 per transform row n1 < N1/2
+  constexpr int RK = E1 <= 4 ? 4 : (E1 <= 8 ? 2 : 0);  // ranks preloaded (register budget)
+  double nn[NO], u[RK > 0 ? RK : 1][NO], w[RK > 0 ? RK : 1];
+#pragma unroll
+  for (int q = 0; q < NO; ++q) {
+    const int64_t jo = (int64_t)(j + (q >> 1) * T1) * N2 + col + 1 + (q & 1);  // out index = conv index + 1
+    const bool ok = rs && jo < m;
+    nn[q] = ok ? n[jo] : 0.0;
+#pragma unroll
+    for (int k = 0; k < RK; ++k) u[k][q] = (ok && k < a.r) ? __ldg(a.ut + (int64_t)k * m + jo) : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < RK; ++k) w[k] = (rs && k < a.r) ? a.scalars[k] : 0.0;
+  (void)w;
   __syncthreads();
   block_fft<N1, E1, +1, false, kNoPad>(v, smem + c * RG, j, smtw);
-  const double* __restrict__ n = a.n.get();
   const double scale = ldexp(0.5, -a.log2p);
 #pragma unroll
-  for (int r = 0; r < E1 / 2; ++r) {
-    const int64_t base = (int64_t)(j + r * T1) * N2 + col + 1;  // out index = conv index + 1
-    if (base < m) a.out[base] = epilogue(a, n, base, scale * v[r].x);
-    if (base + 1 < m) a.out[base + 1] = epilogue(a, n, base + 1, scale * v[r].y);
+  for (int q = 0; q < NO; ++q) {
+    const int64_t jo = (int64_t)(j + (q >> 1) * T1) * N2 + col + 1 + (q & 1);
+    if (jo < m) {
+      double rowsum = 0.0;  // rank order, as rhs.cpp:24-46
+      if (rs) {
+#pragma unroll
+        for (int k = 0; k < RK; ++k)
+          if (k < a.r) rowsum += u[k][q] * w[k];
+        for (int ra = RK; ra < a.r; ++ra) rowsum += __ldg(a.ut + (int64_t)ra * m + jo) * a.scalars[ra];
+      }
+      a.out[jo] = epilogue_rsn(a, nn[q], jo, scale * ((q & 1) ? v[q >> 1].y : v[q >> 1].x), rowsum);
+    }
   }
   if (blockIdx.x == 0 && tid == 0) a.out[0] = epilogue0(a, n);
   pdl_trigger();
@@ -509,7 +540,8 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
     AGK_CK(launch_k(k_col_fwd<CF::N1, CF::E1, CF::C>, CF::N2 / CF::C, CF::C * CF::T1, sm1, s, pdl, a, g0, gc));
     mark(mk, K_COL_FWD, s);
-    AGK_CK(launch_k(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, CF::N1 / 2 + 1, 2 * CF::T2, sm2, s, pdl, a, g0,
+    AGK_CK(launch_k(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, CF::N1 / 2 + 1 + (g0 + gc >= a.rf ? 1 : 0),
+                    2 * CF::T2, sm2, s, pdl, a, g0,
                     gc, (int)(g0 == 0), (int)(g0 + gc >= a.rf)));
     mark(mk, K_ROW, s);
   }
