@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   // immutable operands (U, V, tables) first: they overlap the predecessor's tail
   if (gcount > 0) prefetch(g0);
   load_twiddles<N1, E1>(smtw, a.tw_n1);
+  const TwSeries<-1> tw0(a.twp, (uint32_t)(n2 * j), (uint32_t)(n2 * T1));  // four-step twiddles
   pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
   if (a.skip && *a.skip) {
     cp_async_wait_all();
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
     __syncthreads();  // twiddle tables ready / previous rank's smem reads done
     block_fft<N1, E1, -1, true, kNoPad>(v, sm, j, smtw);
     double2* __restrict__ yg = a.y + (int64_t)g * P;
-    TwSeries<-1> tw(a.twp, (uint32_t)(n2 * j), (uint32_t)(n2 * T1));
+    TwSeries<-1> tw = tw0;
 #pragma unroll
     for (int r = 0; r < E1; ++r) {
       const int64_t k1 = j + r * T1;
@@ -260,11 +261,12 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
   double2* smtw = smem + 2 * PL::SMEM;
   double2* stage = smtw + PL::TWS;  // [E2][NT]: this thread's elements of the next rank's row
   load_twiddles<N2, E2>(smtw, a.tw_n2);  // immutable table: overlaps the predecessor's tail
-  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
-  if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, team = tid / T2, j = tid % T2;
   const int n1 = a.n1;
   const int k1 = blockIdx.x;
+  const TwSeries<+1> itw0(a.twp, (uint32_t)(j * k1), (uint32_t)(T2 * k1));  // inverse four-step twiddles
+  pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
+  if (a.skip && *a.skip) return;
   const int row = team == 0 ? k1 : (n1 - k1) & (n1 - 1);
   const int64_t P = (int64_t)n1 * N2;
   auto prefetch = [&](int g) {
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
   __syncthreads();
   block_fft<N2, E2, +1, false>(u, smem, j, smtw, act);
   if (act) {
-    TwSeries<+1> tw(a.twp, (uint32_t)(j * k1), (uint32_t)(T2 * k1));
+    TwSeries<+1> tw = itw0;
 #pragma unroll
     for (int r = 0; r < E2; ++r) {
       const int64_t c2 = j + r * T2;
