@@ -210,6 +210,16 @@ struct HandleRhs final : RhsEnqueue {
     return rhs_launch(h->plan, a, s);
   }
   int launches() const override { return h->kind == AGK_RHS_MODEL ? h->plan.launches : 1; }
+  bool stage_fusable() const override { return h->kind == AGK_RHS_MODEL && !h->plan.dense && knob("AGK_FUSE_STAGES", 1) != 0; }
+  cudaError_t stage(VecRef x, const StageIn& st, double* stg, double* out, cudaStream_t s) const override {
+    RhsArgs a = h->base;
+    a.n = x;
+    a.st = st;
+    a.stg_out = stg;
+    a.out = out;
+    a.skip = nullptr;
+    return rhs_launch(h->plan, a, s);
+  }
 };
 
 int body_for(const agk_control* c) {

@@ -9,6 +9,7 @@
 
 #include "agk/agk.h"
 #include "fft.cuh"
+#include "stage.cuh"
 
 namespace agk {
 
@@ -33,7 +34,9 @@ struct VecRef {
 
 // Everything an RHS evaluation needs, by value in every kernel.
 struct RhsArgs {
-  VecRef n;             // input state (m)
+  VecRef n;             // input state (m); with a fused stage (st.on): the stage's base x
+  StageIn st;           // fused RK stage: the RHS input is n + tau * sum a_j y_j (stage.cuh)
+  double* stg_out;      // fused stage: the first kernel stores the stage vector here (m) for the others
   double* out;          // output S(n) (m)
   const int* skip;      // if non-null and *skip != 0 the whole evaluation is skipped
   int64_t m;

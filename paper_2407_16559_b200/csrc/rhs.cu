@@ -56,7 +56,13 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
   load_twiddles<P, E>(smtw, a.tw_small);
   const int tid = threadIdx.x;
   const int64_t m = a.m;
-  const double* __restrict__ n = a.n.get();
+  if (a.st.on) {  // fused RK stage: form the stage vector once (visible to the CTA after the barrier)
+    const double* x = a.n.get();
+    const double t = a.st.tau_mul * *a.st.tau;
+    for (int64_t i = tid; i < m; i += NT) a.stg_out[i] = stage_at(a.st, t, x[i], i);
+    __syncthreads();
+  }
+  const double* __restrict__ n = a.st.on ? a.stg_out : a.n.get();
   const bool act = tid < T;
   double2 acc[QA];
 #pragma unroll
@@ -208,10 +214,22 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   }
   const double* __restrict__ n = a.n.get();
   double nl[H];
+  if (a.st.on) {
+    // fused RK stage: n_i = x_i + tau sum_j a_j k_j[i] formed here (each i by one thread) and
+    // stored for the row and inverse-column kernels
+    const double t = a.st.tau_mul * *a.st.tau;
 #pragma unroll
-  for (int r = 0; r < H; ++r) {
-    const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
-    nl[r] = i < m ? n[i] : 0.0;
+    for (int r = 0; r < H; ++r) {
+      const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
+      nl[r] = i < m ? stage_at(a.st, t, n[i], i) : 0.0;
+      if (i < m) a.stg_out[i] = nl[r];
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < H; ++r) {
+      const int64_t i = (int64_t)(j + r * T1) * N2 + n2;
+      nl[r] = i < m ? n[i] : 0.0;
+    }
   }
   double2* sm = smem + c * RG;
   for (int g = 0; g < gcount; ++g) {
@@ -525,6 +543,17 @@ int pdl_mask() {
   return m;
 }
 
+// A fused RK stage (a.st.on): only the first kernel of an RHS forms the stage (and stores it to
+// a.stg_out); the others read the stored vector.
+static RhsArgs rest_args(const RhsArgs& a) {
+  RhsArgs r = a;
+  if (a.st.on) {
+    r.st.on = 0;
+    r.n = VecRef{a.stg_out, nullptr, 0};
+  }
+  return r;
+}
+
 template <int P>
 static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s, Marks* mk) {
   AGK_CK(launch_k(k_small<P>, 1, SmallCfg<P>::NT, SmallCfg<P>::SMEM_BYTES, s, !mk && pdl_enabled() && (pdl_mask() & 32), a));
@@ -534,13 +563,15 @@ static cudaError_t launch_small(const RhsArgs& a, cudaStream_t s, Marks* mk) {
 
 template <typename CF>
 static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, Marks* mk) {
-  RhsArgs a = a0;
-  a.nblk_colfwd = CF::N2 / CF::C;
+  RhsArgs first = a0;
+  first.nblk_colfwd = CF::N2 / CF::C;
+  const RhsArgs a = rest_args(first);
   const size_t sm1 = CF::SM_COLFWD, sm2 = CF::SM_ROW, sm3 = CF::SM_COLINV;
   const bool pdl = !mk && pdl_enabled() && (pdl_mask() & (CF::N1 * CF::N2 <= 8192 ? 64 : 32));
   for (int g0 = 0; g0 < a.rf; g0 += p.gsize) {
     const int gc = (a.rf - g0) < p.gsize ? (a.rf - g0) : p.gsize;
-    AGK_CK(launch_k(k_col_fwd<CF::N1, CF::E1, CF::C>, CF::N2 / CF::C, CF::C * CF::T1, sm1, s, pdl, a, g0, gc));
+    AGK_CK(launch_k(k_col_fwd<CF::N1, CF::E1, CF::C>, CF::N2 / CF::C, CF::C * CF::T1, sm1, s, pdl,
+                    g0 == 0 ? first : a, g0, gc));
     mark(mk, K_COL_FWD, s);
     AGK_CK(launch_k(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, CF::N1 / 2 + 1 + (g0 + gc >= a.rf ? 1 : 0),
                     2 * CF::T2, sm2, s, pdl, a, g0,
@@ -605,7 +636,10 @@ static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStre
 }
 
 static cudaError_t rhs_launch_impl(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
-  if (p.dense) return rhs_dense_launch(p, a, s, mk ? mark_cb : nullptr, mk);
+  if (p.dense) {
+    if (a.st.on) return cudaErrorInvalidValue;  // no fused stages on the dense path (rhs_stage_fusable)
+    return rhs_dense_launch(p, a, s, mk ? mark_cb : nullptr, mk);
+  }
   if (p.fast) return rhs_w_launch(p, a, s, mk ? mark_cb : nullptr, mk);
   switch (p.log2p) {
     case 2: return launch_small<4>(a, s, mk);

@@ -77,10 +77,22 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
   const int bx = blockIdx.x % (kW_N2 / 64), by = blockIdx.x / (kW_N2 / 64);  // n2 tile, n1 tile
   const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
   double v[16];
+  if (a.st.on) {
+    // fused RK stage: n_i = x_i + tau sum_j a_j k_j[i], formed here and also stored in natural
+    // layout (the D kernel reads it)
+    const double t = a.st.tau_mul * *a.st.tau;
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    const int64_t i = (int64_t)(by * 64 + ty + 4 * q) * kW_N2 + bx * 64 + tx;
-    v[q] = i < a.m ? n[i] : 0.0;
+    for (int q = 0; q < 16; ++q) {
+      const int64_t i = (int64_t)(by * 64 + ty + 4 * q) * kW_N2 + bx * 64 + tx;
+      v[q] = i < a.m ? stage_at(a.st, t, n[i], i) : 0.0;
+      if (i < a.m) a.stg_out[i] = v[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t i = (int64_t)(by * 64 + ty + 4 * q) * kW_N2 + bx * 64 + tx;
+      v[q] = i < a.m ? n[i] : 0.0;
+    }
   }
 #pragma unroll
   for (int q = 0; q < 16; ++q) t[ty + 4 * q][tx] = v[q];
@@ -644,12 +656,18 @@ cudaError_t rhs_w_set_smem_limits() {
 // programmatic dependent of the one before (pdl_entry in every kernel; off under timing marks).
 cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, void (*mark)(void*, int, cudaStream_t),
                          void* mk) {
-  RhsArgs a = a0;
-  a.dbg = knob("AGK_DBG", 0);  // experiment switches (tools/ab.sh): AGK_EXPERIMENTS builds only
-  a.pfd = knob("AGK_PFD", 1);  // L2 prefetch distance (items)
+  RhsArgs first = a0;
+  first.dbg = knob("AGK_DBG", 0);  // experiment switches (tools/ab.sh): AGK_EXPERIMENTS builds only
+  first.pfd = knob("AGK_PFD", 1);  // L2 prefetch distance (items)
+  // a fused RK stage is formed by the transpose; the later kernels read the stored stage vector
+  RhsArgs a = first;
+  if (a.st.on) {
+    a.st.on = 0;
+    a.n = VecRef{a.stg_out, nullptr, 0};
+  }
   const int nsm = p.nsm > 0 ? p.nsm : 148;
   const bool pdl = !mark && pdl_enabled();
-  AGK_CK(launch_k(k_transpose_n, (kW_H / 64) * (kW_N2 / 64), 256, 0, s, pdl && (pdl_mask() & 1), a));
+  AGK_CK(launch_k(k_transpose_n, (kW_H / 64) * (kW_N2 / 64), 256, 0, s, pdl && (pdl_mask() & 1), first));
   if (mark) mark(mk, K_TRANSPOSE, s);
   a.nblk_colfwd = kW_N2 / 8;
   const int rows = kW_N1 / 2 + 1;

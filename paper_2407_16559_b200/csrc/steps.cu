@@ -20,30 +20,9 @@
 
 namespace agk {
 
-namespace rkf {
-constexpr double a21 = 1.0 / 4.0;
-constexpr double a31 = 3.0 / 32.0, a32 = 9.0 / 32.0;
-constexpr double a41 = 1932.0 / 2197.0, a42 = -7200.0 / 2197.0, a43 = 7296.0 / 2197.0;
-constexpr double a51 = 439.0 / 216.0, a52 = -8.0, a53 = 3680.0 / 513.0, a54 = -845.0 / 4104.0;
-constexpr double a61 = -8.0 / 27.0, a62 = 2.0, a63 = -3544.0 / 2565.0, a64 = 1859.0 / 4104.0, a65 = -11.0 / 40.0;
-constexpr double b5_0 = 16.0 / 135.0, b5_2 = 6656.0 / 12825.0, b5_3 = 28561.0 / 56430.0, b5_4 = -9.0 / 50.0,
-                 b5_5 = 2.0 / 55.0;
-constexpr double b4_0 = 25.0 / 216.0, b4_2 = 1408.0 / 2565.0, b4_3 = 2197.0 / 4104.0, b4_4 = -1.0 / 5.0;
-}  // namespace rkf
-
 constexpr double kErrFloor = 1e-300;             // steppers.cpp:11
 constexpr double kNegativeRejectFraction = 1e-3; // steppers.cpp:14
 constexpr int kRedThreads = 256;
-
-enum CombKind {
-  C_RK2_ST,   // x + t*y0                                    (steppers.cpp:103)
-  C_RK2_OUT,  // x + 0.5*t*(y0 + y1)                         (steppers.cpp:105)
-  C_RK4_STH,  // x + 0.5*t*y0                                (steppers.cpp:113,115)
-  C_RK4_ST1,  // x + t*y0                                    (steppers.cpp:117)
-  C_RK4_OUT,  // x + t*(y0 + 2 y1 + 2 y2 + y3)/6             (steppers.cpp:119-121)
-  C_F2, C_F3, C_F4, C_F5, C_F6,                            // (steppers.cpp:130-147)
-  C_F_OUT     // n4 (stored) and n5 (reduced / optional)     (steppers.cpp:149-158)
-};
 
 struct OutRef {
   double* base;
@@ -71,14 +50,7 @@ struct CombArgs {
 
 __device__ __forceinline__ bool finite_d(double x) { return isfinite(x); }
 
-// stage-vector inputs of each combination and the y slot each comes from
-__host__ __device__ constexpr int comb_inputs(int kind) {
-  return kind == C_RK2_ST || kind == C_RK4_STH || kind == C_RK4_ST1 || kind == C_F2 ? 1
-         : kind == C_RK2_OUT || kind == C_F3                                      ? 2
-         : kind == C_F4                                                           ? 3
-         : kind == C_RK4_OUT || kind == C_F5                                      ? 4
-                                                                                  : 5;  // C_F6, C_F_OUT
-}
+// the y slot each input of a combination comes from
 __host__ __device__ constexpr int comb_slot(int kind, int j) { return kind == C_F_OUT && j > 0 ? j + 1 : j; }
 
 template <int KIND, bool RED>
@@ -101,23 +73,10 @@ __global__ void __launch_bounds__(kRedThreads) k_comb(CombArgs a) {
     double o;
     other = 0.0;
     using namespace rkf;
-    switch (KIND) {
-      case C_RK2_ST: o = xi + t * yy[0]; break;
-      case C_RK2_OUT: o = xi + 0.5 * t * (yy[0] + yy[1]); break;
-      case C_RK4_STH: o = xi + 0.5 * t * yy[0]; break;
-      case C_RK4_ST1: o = xi + t * yy[0]; break;
-      case C_RK4_OUT: o = xi + t * (yy[0] + 2.0 * yy[1] + 2.0 * yy[2] + yy[3]) / 6.0; break;
-      case C_F2: o = xi + t * a21 * yy[0]; break;
-      case C_F3: o = xi + t * (a31 * yy[0] + a32 * yy[1]); break;
-      case C_F4: o = xi + t * (a41 * yy[0] + a42 * yy[1] + a43 * yy[2]); break;
-      case C_F5: o = xi + t * (a51 * yy[0] + a52 * yy[1] + a53 * yy[2] + a54 * yy[3]); break;
-      case C_F6: o = xi + t * (a61 * yy[0] + a62 * yy[1] + a63 * yy[2] + a64 * yy[3] + a65 * yy[4]); break;
-      default: {  // C_F_OUT: inputs k1, k3, k4, k5, k6
-        const double k1 = yy[0], k3 = yy[1], k4 = yy[2], k5 = yy[3], k6 = yy[4];
-        other = xi + t * (b5_0 * k1 + b5_2 * k3 + b5_3 * k4 + b5_4 * k5 + b5_5 * k6);
-        o = xi + t * (b4_0 * k1 + b4_2 * k3 + b4_3 * k4 + b4_4 * k5);
-        break;
-      }
+    if constexpr (KIND == C_F_OUT) {  // inputs k1, k3, k4, k5, k6
+      comb_f_out(t, xi, yy, o, other);
+    } else {
+      o = comb_value<KIND>(t, xi, yy);  // the same expression as a fused stage (stage.cuh)
     }
     const double n5v = other;
     if (RED) {
@@ -657,19 +616,44 @@ cudaError_t build_step_graph(int body, int stepper, const RhsEnqueue& rhs, const
     return r;
   };
   auto plain = [](const double* p) { return VecRef{p, nullptr, 0}; };
+  // RHS of the stage x + tau * tmul * sum_j a_j ys[j] (CombKind `kind`): fused into the RHS's first
+  // kernel when the RHS supports it, else a stage-combination pass into b.stg and the RHS of b.stg
+  const bool fuse = rhs.stage_fusable();
+  int nfused = 0;
+  auto stage_rhs = [&](int kind, VecRef x, std::initializer_list<const double*> ys, double tmul,
+                       double* out) -> cudaError_t {
+    if (fuse) {
+      StageIn st{};
+      st.on = 1;
+      st.kind = kind;
+      int q = 0;
+      for (const double* y : ys) st.y[q++] = y;
+      st.tau = &ctl->tau;
+      st.tau_mul = tmul;
+      ++nfused;
+      return rhs.stage(x, st, b.stg, out, s);
+    }
+    const CombArgs ca2 = st_args(x, b.stg, ys, tmul);
+    switch (kind) {
+      case C_RK2_ST: AGK_CK((comb<C_RK2_ST, false>(ca2, nb, s))); break;
+      case C_RK4_STH: AGK_CK((comb<C_RK4_STH, false>(ca2, nb, s))); break;
+      case C_RK4_ST1: AGK_CK((comb<C_RK4_ST1, false>(ca2, nb, s))); break;
+      case C_F2: AGK_CK((comb<C_F2, false>(ca2, nb, s))); break;
+      case C_F3: AGK_CK((comb<C_F3, false>(ca2, nb, s))); break;
+      case C_F4: AGK_CK((comb<C_F4, false>(ca2, nb, s))); break;
+      case C_F5: AGK_CK((comb<C_F5, false>(ca2, nb, s))); break;
+      default: AGK_CK((comb<C_F6, false>(ca2, nb, s))); break;
+    }
+    return rhs(plain(b.stg), out, nullptr, s);
+  };
 
   if (body == BODY_FEHLBERG) {
     AGK_CK(rhs(state, K[0], k1skip, s));
-    AGK_CK(comb<C_F2, false>(st_args(state, b.stg, {K[0]}, 1.0), nb, s));
-    AGK_CK(rhs(plain(b.stg), K[1], nullptr, s));
-    AGK_CK(comb<C_F3, false>(st_args(state, b.stg, {K[0], K[1]}, 1.0), nb, s));
-    AGK_CK(rhs(plain(b.stg), K[2], nullptr, s));
-    AGK_CK(comb<C_F4, false>(st_args(state, b.stg, {K[0], K[1], K[2]}, 1.0), nb, s));
-    AGK_CK(rhs(plain(b.stg), K[3], nullptr, s));
-    AGK_CK(comb<C_F5, false>(st_args(state, b.stg, {K[0], K[1], K[2], K[3]}, 1.0), nb, s));
-    AGK_CK(rhs(plain(b.stg), K[4], nullptr, s));
-    AGK_CK(comb<C_F6, false>(st_args(state, b.stg, {K[0], K[1], K[2], K[3], K[4]}, 1.0), nb, s));
-    AGK_CK(rhs(plain(b.stg), K[5], nullptr, s));
+    AGK_CK(stage_rhs(C_F2, state, {K[0]}, 1.0, K[1]));
+    AGK_CK(stage_rhs(C_F3, state, {K[0], K[1]}, 1.0, K[2]));
+    AGK_CK(stage_rhs(C_F4, state, {K[0], K[1], K[2]}, 1.0, K[3]));
+    AGK_CK(stage_rhs(C_F5, state, {K[0], K[1], K[2], K[3]}, 1.0, K[4]));
+    AGK_CK(stage_rhs(C_F6, state, {K[0], K[1], K[2], K[3], K[4]}, 1.0, K[5]));
     CombArgs fa = st_args(state, nullptr, {K[0], K[1], K[2], K[3], K[4], K[5]}, 1.0);
     fa.out = cand;
     AGK_CK(comb<C_F_OUT, true>(fa, nb, s));
@@ -685,18 +669,14 @@ cudaError_t build_step_graph(int body, int stepper, const RhsEnqueue& rhs, const
       }
       CombArgs fa{};
       if (stepper == AGK_RK2) {
-        AGK_CK(comb<C_RK2_ST, false>(st_args(x, b.stg, {k1buf}, tmul), nb, s));
-        AGK_CK(rhs(plain(b.stg), K[1], nullptr, s));
+        AGK_CK(stage_rhs(C_RK2_ST, x, {k1buf}, tmul, K[1]));
         fa = st_args(x, out_plain, {k1buf, K[1]}, tmul);
         nk += 2;
         nrhs += 1;
       } else {
-        AGK_CK(comb<C_RK4_STH, false>(st_args(x, b.stg, {k1buf}, tmul), nb, s));
-        AGK_CK(rhs(plain(b.stg), K[1], nullptr, s));
-        AGK_CK(comb<C_RK4_STH, false>(st_args(x, b.stg, {K[1]}, tmul), nb, s));
-        AGK_CK(rhs(plain(b.stg), K[2], nullptr, s));
-        AGK_CK(comb<C_RK4_ST1, false>(st_args(x, b.stg, {K[2]}, tmul), nb, s));
-        AGK_CK(rhs(plain(b.stg), K[3], nullptr, s));
+        AGK_CK(stage_rhs(C_RK4_STH, x, {k1buf}, tmul, K[1]));
+        AGK_CK(stage_rhs(C_RK4_STH, x, {K[1]}, tmul, K[2]));
+        AGK_CK(stage_rhs(C_RK4_ST1, x, {K[2]}, tmul, K[3]));
         fa = st_args(x, out_plain, {k1buf, K[1], K[2], K[3]}, tmul);
         nk += 4;
         nrhs += 3;
@@ -729,7 +709,7 @@ cudaError_t build_step_graph(int body, int stepper, const RhsEnqueue& rhs, const
   AGK_CK(cudaStreamEndCapture(s, &bg));
   AGK_CK(cudaGraphInstantiate(exec, g, 0));
   AGK_CK(cudaGraphDestroy(g));
-  if (kernels_per_trial) *kernels_per_trial = nk + nrhs * rhs.launches();
+  if (kernels_per_trial) *kernels_per_trial = nk - nfused + nrhs * rhs.launches();
   return cudaSuccess;
 }
 

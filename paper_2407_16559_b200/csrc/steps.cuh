@@ -73,6 +73,10 @@ struct StepBuffers {
 struct RhsEnqueue {
   virtual cudaError_t operator()(VecRef in, double* out, const int* skip, cudaStream_t s) const = 0;
   virtual int launches() const = 0;  // kernels one call enqueues
+  // Fused stage: one RHS of the stage x + tau * sum_j a_j y_j (StageIn) whose first kernel forms
+  // the stage itself and stores it to stg, in place of a stage-combination kernel + RHS(stg).
+  virtual bool stage_fusable() const { return false; }
+  virtual cudaError_t stage(VecRef, const StageIn&, double*, double*, cudaStream_t) const { return cudaErrorNotSupported; }
   virtual ~RhsEnqueue() = default;
 };
 
