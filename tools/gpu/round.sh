@@ -1,3 +1,5 @@
+# full GPU round: smoke, pytest -m gpu (parity report to gpurun_out/parity_$TAG.jsonl), bench
+mkdir -p gpurun_out
 export AGK_PARITY_REPORT=gpurun_out/parity_${TAG:-r02a}.jsonl; rm -f $AGK_PARITY_REPORT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_${TAG:-r02a}.txt 2>&1
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${TAG:-r02a}.log 2>&1
