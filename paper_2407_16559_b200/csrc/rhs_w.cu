@@ -699,7 +699,8 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     // measured at M = 2^20 (tools/timeline.py), row ~ 20 + 9.6 rf us and D on 19 SMs ~ 65 + 4 r us.
     const int free = nsm - rgrid;
     const size_t dsm = (size_t)(4 * a.rf + 3 * a.r + 2) * sizeof(double);
-    if (9.6 * a.rf >= 45.0 + 4.0 * a.r && free >= 8) {
+    const int dmode = knob("AGK_DVEC_MODE", 0);  // experiments: 1 beside, 2 after (0: the measured rule)
+    if ((dmode == 1 || (dmode == 0 && 9.6 * a.rf >= 45.0 + 4.0 * a.r)) && free >= 8) {
       // every k_dvec CTA must be resident from the start: a CTA that finished early would otherwise
       // hold its SM slot in the final wait for the row grid, and the rest of D would run after it
       AGK_CK(launch_k(k_dvec, 2 * free, 256, dsm, s, !mark, a));
