@@ -41,3 +41,13 @@ def test_no_gpu_raises_instead_of_computing():
     r = _run(code, {})
     assert r.returncode == 0, r.stderr
     assert "RAISED" in r.stdout and "COMPUTED" not in r.stdout, r.stdout
+
+
+def test_production_library_reads_no_experiment_knobs():
+    """the AGK_* experiment switches (tools/ab.sh) exist only in the
+    -DAGK_EXPERIMENTS build (libagk_b200_exp.so); the production library cannot see them, so no
+    stray environment variable can change a plan or skip work in a timed or parity run."""
+    blob = open(os.path.join(ROOT, "paper_2407_16559_b200", "libagk_b200.so"), "rb").read()
+    for knob in (b"AGK_DBG", b"AGK_PFD", b"AGK_FAST", b"AGK_RANK_GROUP", b"AGK_PDL", b"AGK_VARIANT", b"AGK_MVAR",
+                 b"AGK_FUSE_STAGES", b"AGK_DVEC_MODE"):
+        assert knob not in blob, knob
