@@ -51,20 +51,40 @@ def summarize_state(x):
     return dict(N=float(x.sum()), M1=float(np.dot(k, x)), accepted=None, full=x)
 
 
+def entries(run):
+    """(indices, values) a run's state is compared at: the head (everything above 1e-13 max n),
+    or for compacted goldens the first 2^17 entries plus every 16th beyond (make_parity_runs)."""
+    if "full" in run:
+        x = run["full"]
+        return np.arange(x.size), x
+    head = np.asarray(run["head"], dtype=np.float64)
+    idx = np.arange(head.size)
+    if "sample_idx" in run:
+        return np.concatenate([idx, run["sample_idx"]]), np.concatenate([head, run["sample_val"]])
+    return idx, head
+
+
+def head_len(run):
+    return int(run["head_len"]) if "head_len" in run else int(np.asarray(run["head"]).size)
+
+
 def distance(got, want):
     """north_star quantities of run `got` against the reference run `want` (golden dict)."""
-    head = np.asarray(want["head"], dtype=np.float64)
-    h = head.size
+    wi, wv = entries(want)
+    h = head_len(want)
     maxn = float(want["maxn"])
+    gi, gv = entries(got)
+    lut = dict(zip(gi.tolist(), gv.tolist())) if "full" not in got else None
     if "full" in got:
         g = got["full"]
-        gh, gtail = g[:h], (float(np.max(np.abs(g[h:]))) if g.size > h else 0.0)
-    else:  # another golden: its own head (zero-padded) and tail bound
-        g = np.asarray(got["head"], dtype=np.float64)
-        gh = np.zeros(h)
-        gh[: min(h, g.size)] = g[:h]
-        gtail = max(float(got["tail_maxabs"]), float(np.max(np.abs(g[h:]))) if g.size > h else 0.0)
-    dn = max(float(np.max(np.abs(gh - head))) if h else 0.0, gtail + float(want["tail_maxabs"]))
+        gvals = g[wi]
+        gtail = float(np.max(np.abs(g[h:]))) if g.size > h else 0.0
+    else:  # another golden: its value at the reference's kept entries (0 past its own head)
+        gvals = np.array([lut.get(i, 0.0) for i in wi.tolist()])
+        gtail = float(got["tail_maxabs"])
+    head = wv
+    gh = gvals
+    dn = max(float(np.max(np.abs(gh - head))) if head.size else 0.0, gtail + float(want["tail_maxabs"]))
     big = head > 1e-9 * maxn
     return dict(
         N=abs(float(got["N"]) - float(want["N"])) / abs(float(want["N"])),
