@@ -284,6 +284,143 @@ __global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) 
 
 
 
+// Column pass with the transposition done by the transform's own exchange (no output tile):
+// step A as in k_colt (warp w = column w of the octet, lane = l), exchanged through the CTA's
+// 1024 x 8 tile, but step B is dealt across the CTA by (column, k): lane (c = lane & 7,
+// kk = lane >> 3) of warp w' runs the radix-32 DFT over l of column c at k = 4 w' + kk and so
+// holds X_c[k + 32 q], q < 32. A warp store at fixed q is then 4 rows (k .. k+3... one per kk) of
+// 8 consecutive slots = four full 128-byte Y lines straight from registers: the tile write-back
+// (32 STS.128 + 32 LDS.128 per thread and item) and the wait for the tile to drain are gone.
+// Same arithmetic per element as k_colt (bitwise the same Y).
+__global__ void __launch_bounds__(256, 1) k_colx(RhsArgs a, int g0, int gcount) {
+  tl_mark(a, 1, 0);
+  extern __shared__ double2 smem[];
+  double2* T = smem;               // 1024 x 8 exchange tile (tile_idx)
+  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
+  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
+  double2* tq = tw + 1024;         // [4][256]: four-step chain heads W_P^{n2 (k + 32 j)} of this thread's (column, k)
+  __shared__ double red[2][8][4];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int cB = lane & 7, kB = 4 * w + (lane >> 3);  // step-B role
+  const int items = (kW_N2 / 8) * gcount;
+  const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
+  const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
+  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
+  double2* Sw = S + w * kW_H;
+  auto col_of = [&](int o, int c) { return 16 * (o >> 1) + 2 * c + (o & 1); };
+  auto prefetch = [&](int item) {
+    const int o = item / gcount, ub = g0 + item % gcount;
+    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + col_of(o, w)) * kW_H;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
+    cp_async_commit();
+  };
+  if (it0 < it1) prefetch(it0);
+  __syncthreads();
+  pdl_entry();  // programmatic dependent of the transpose of n (ng is read only from here on)
+  tl_mark(a, 1, 1);
+  if (a.skip && *a.skip) {
+    cp_async_wait_all();
+    return;
+  }
+  double nl[16];
+  double2 stB = czero();
+  int cur_o = -1;
+  for (int item = it0; item < it1; ++item) {
+    const int o = item / gcount, g = item % gcount, ub = g0 + g;
+    const int n2 = col_of(o, w);
+    if (o != cur_o) {
+      cur_o = o;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
+      // four-step factors of the step-B role: W_P^{n2B k1}, k1 = kB + 32 q, as four chains
+      // t_{j+4m} = (W_P^{n2B kB} W_P^{32 n2B j}) (W_P^{128 n2B})^m (the factors k_colt forms)
+      const int n2B = col_of(o, cB);
+      const double2 base = tw_p<-1>(a.twp, (uint32_t)(n2B * kB));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tq[j * 256 + tid] = cmul(base, tw_p<-1>(a.twp, (uint32_t)(32 * n2B * j)));
+      stB = tw_p<-1>(a.twp, (uint32_t)(32 * n2B * 4));
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    double2 v[32];
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const double2 uv = Sw[lane + 32 * r];
+      const double x = uv.x * nl[r], y = uv.y * nl[r];
+      v[r] = make_double2(x, y);
+      const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
+      if (i >= 1) {
+        const double sz = (double)(i + 1);
+        s0 += x;
+        s1 += sz * x;
+        s2 += y;
+        s3 += sz * y;
+      }
+    }
+    __syncwarp();
+    if (item + 1 < it1) prefetch(item + 1);
+    {
+      // step A: radix-32 DFT over r with the upper half zero, as two radix-16 DFTs
+      double2 ea[16], ob[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        ea[r] = v[r];
+        ob[r] = mul_w32<-1>(v[r], r);
+      }
+      Dft<16, -1>::run(ea);
+      Dft<16, -1>::run(ob);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        v[2 * k] = ea[k];
+        v[2 * k + 1] = ob[k];
+      }
+      twiddle_a_rec<-1>(v, tw, lane);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    s3 = warp_sum(s3);
+    if (lane == 0) {
+      double* rd = red[item & 1][w];
+      rd[0] = s0;
+      rd[1] = s1;
+      rd[2] = s2;
+      rd[3] = s3;
+    }
+    __syncthreads();  // every thread has read the previous item's exchange
+#pragma unroll
+    for (int k = 0; k < 32; ++k) T[tile_idx(32 * k + lane, w)] = v[k];
+    __syncthreads();
+    if (tid < 4) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) t += red[item & 1][q][tid];
+      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
+    }
+    // step B in the (column, k) role
+#pragma unroll
+    for (int l = 0; l < 32; ++l) v[l] = T[tile_idx(32 * kB + l, cB)];
+    Dft<32, -1>::run(v);
+    double2 t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[j] = tq[j * 256 + tid];
+    // rows kB + 32 q, slots (o & 1) * 1024 + 8 (o >> 1) + cB of rank g
+    double2* __restrict__ yq = a.y + (int64_t)g * kW_YP + (int64_t)kB * kW_YS + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1) + cB;
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) yq[(int64_t)(4 * mm + j) * 32 * kW_YS] = cmul(v[4 * mm + j], t[j]);
+      if (mm < 7) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) t[j] = cmul(t[j], stB);
+      }
+    }
+  }
+  tl_mark(a, 1, 2);
+}
+
 // Row pass: a CTA is two independent halves of 4 warps (named barriers 1 and 2), each owning one
 // row pair (k1, N1-k1) at a time with warps (rho, h) = (row, even/odd samples). Per rank a warp
 // loads its 1024 samples (contiguous: the permuted Y layout) and transforms them to E (h = 0) or
@@ -623,6 +760,7 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
 }
 
 static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
+static size_t smem_colx() { return smem_colt() + (size_t)4 * 256 * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
 template <int CW>
 static size_t smem_colinvw_t() {
@@ -642,6 +780,7 @@ cudaError_t rhs_w_set_smem_limits() {
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
   SET(k_colt<0>, smem_colt());
   SET(k_colt<1>, smem_colt());
+  SET(k_colx, smem_colx());
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
   SET(k_colinvw<8>, smem_colinvw());
@@ -679,8 +818,10 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
     const int cgrid = items < nsm ? items : nsm;
-    static const int stv = knob("AGK_STV", 1);  // 1: measured -3.5 us
-    if (stv == 1) {
+    static const int stv = knob("AGK_STV", 2);  // 2: transposing step B; 1: tile write-back in quarters
+    if (stv == 2) {
+      AGK_CK(launch_k(k_colx, cgrid, 256, smem_colx(), s, pdl && (pdl_mask() & 2), a, g0, gc));
+    } else if (stv == 1) {
       AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     } else {
       AGK_CK(launch_k(k_colt<0>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
