@@ -384,6 +384,39 @@ __device__ __forceinline__ void twiddle_a_rec(double2 (&v)[32], const double2* t
     }
   }
 }
+// the same, handing each twiddled value to store(k, v[k]) as soon as it is formed (the caller's
+// exchange stores then interleave with the twiddle arithmetic)
+template <int SIGN, class Store>
+__device__ __forceinline__ void twiddle_a_rec_store(double2 (&v)[32], const double2* tw, int lane, Store&& store) {
+  double2 t[4], w4;
+  t[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int j = 1; j < 4; ++j) t[j] = tw[j * 32 + lane];
+  w4 = tw[4 * 32 + lane];
+  if (SIGN > 0) {
+#pragma unroll
+    for (int j = 1; j < 4; ++j) t[j] = cconj(t[j]);
+    w4 = cconj(w4);
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 4 * m + j;
+      if (m == 0 && j == 0) {
+      } else if (m == 1 && j == 0) {
+        v[k] = cmul(v[k], w4);
+      } else {
+        v[k] = cmul(v[k], t[j]);
+      }
+      store(k, v[k]);
+    }
+    if (m < 7) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = (m == 0 && j == 0) ? w4 : cmul(t[j], w4);
+    }
+  }
+}
 template <int SIGN, bool HALFZERO, bool REC = false>
 __device__ __forceinline__ void warp_fft1024(double2 (&v)[32], double2* xs, const double2* tw, int lane) {
   if constexpr (HALFZERO) {

@@ -6,10 +6,11 @@
 // (warp_fft1024: two register radix-32 DFTs around one warp-private shared-memory exchange) —
 // no block-wide barrier inside a transform:
 //   k_transpose_n : n -> column-major grid layout ng (so each column's operands are contiguous)
-//   k_colt        : per (column octet, rank): z = (U_a n, V_a n) from the column-major UV copy
+//   k_colx        : per (column octet, rank): z = (U_a n, V_a n) from the column-major UV copy
 //                   (cp.async prefetch of the next item), 1024-pt forward FFT (upper half zero)
-//                   exchanging inside one swizzled shared tile, four-step twiddle, full-line
-//                   store of the tile into the even/odd-permuted Y rows; moment partials.
+//                   exchanging inside one swizzled shared tile with step B dealt by (column, k), so
+//                   the four-step-twiddled results leave the registers as full 128-byte lines of
+//                   the even/odd-permuted Y rows; moment partials.
 //   k_rowd        : per row pair (k1, N1-k1) x rank: 1024-pt FFTs of the even and odd samples,
 //                   the decimation-in-time radix-2 stage fused into the conjugate-pair split,
 //                   w*A*B summed over ranks in registers. Two independent 4-warp halves per CTA.
@@ -106,192 +107,19 @@ __global__ void __launch_bounds__(256) k_transpose_n(RhsArgs a) {
 // is decimation in time, so each row is stored even/odd-permuted, slot(n2) = (n2 & 1) * 1024 +
 // (n2 >> 1): a row-pass warp then loads its 1024 even or odd samples as contiguous full lines.
 //
-// Column pass: a CTA item is (column octet o, rank): the 8 columns n2 = 16 (o >> 1) + 2 w + (o & 1)
-// (warp w), whose outputs are the 8 consecutive slots (o & 1) * 1024 + 8 (o >> 1) + w of every
-// row. Each warp's 1024-point transform exchanges through, and leaves its twiddled output in, its
-// own chunk of one swizzled 1024 x 8 tile; the CTA then writes the tile back as full 128-byte row
-// lines (4 lines per warp store). Items are rank-minor, so n is reloaded only per octet.
-template <int SV>
-__global__ void __launch_bounds__(256, 1) k_colt(RhsArgs a, int g0, int gcount) {
-  tl_mark(a, 1, 0);
-  extern __shared__ double2 smem[];
-  double2* T = smem;               // 1024 x 8 tile: exchange + output (tile_idx)
-  double2* S = T + 8 * kW_N1;      // 8 staging regions (512 x (U,V))
-  double2* tw = S + 8 * kW_H;      // W_1024^{l k1}, [k1][l]
-  __shared__ double red[8][4];
-  __shared__ double2 tk[8][32];    // four-step factors W_P^{32 n2 k} of the warp's column
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int items = (kW_N2 / 8) * gcount;
-  const int it0 = (int)((int64_t)blockIdx.x * items / gridDim.x);
-  const int it1 = (int)((int64_t)(blockIdx.x + 1) * items / gridDim.x);
-  for (int i = tid; i < 1024; i += blockDim.x) tw[i] = __ldg(a.tw32 + i);
-  double2* Sw = S + w * kW_H;
-  auto col_of = [&](int o) { return 16 * (o >> 1) + 2 * w + (o & 1); };
-  auto prefetch = [&](int item) {
-    const int o = item / gcount, ub = g0 + item % gcount;
-    const double2* src = a.uvg + ((int64_t)ub * kW_N2 + col_of(o)) * kW_H;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) cp_async16(Sw + lane + 32 * r, src + lane + 32 * r);
-    cp_async_commit();
-  };
-  // the tile as full 128-byte row lines: slots (o & 1) * 1024 + 8 (o >> 1) + c of rank g's rows
-  auto store_tile = [&](int item) {
-    const int o = item / gcount, g = item % gcount;
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
-#pragma unroll 8
-    for (int it = 0; it < kW_N1 / 32; ++it) {
-      const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
-      yg[(int64_t)row * kW_YS + c] = T[tile_idx(row, c)];
-    }
-  };
-  // a quarter of the tile (8 lines per thread), fully unrolled: placed between pieces of step A so
-  // the LSU work interleaves with the fp64 work of the transform
-  auto store_quarter = [&](int item, int qtr) {
-    if (item < it0 || AGK_XDBG(a, 2)) return;
-    const int o = item / gcount, g = item % gcount;
-    double2* __restrict__ yg = a.y + (int64_t)g * kW_YP + (o & 1) * (kW_N2 / 2) + 8 * (o >> 1);
-#pragma unroll
-    for (int it = 8 * qtr; it < 8 * qtr + 8; ++it) {
-      const int idx = threadIdx.x + 256 * it, row = idx >> 3, c = idx & 7;
-      yg[(int64_t)row * kW_YS + c] = T[tile_idx(row, c)];
-    }
-  };
-  if (it0 < it1) prefetch(it0);
-  __syncthreads();
-  // launched as a programmatic dependent of the transpose of n: everything above (twiddle table,
-  // first operand prefetch) overlapped it; ng is read only after it completed
-  pdl_entry();
-  tl_mark(a, 1, 1);
-  if (a.skip && *a.skip) {
-    cp_async_wait_all();
-    return;
-  }
-  double nl[16];
-  double2 base = czero();
-  int cur_o = -1;
-  for (int item = it0; item < it1; ++item) {
-    const int o = item / gcount, g = item % gcount, ub = g0 + g;
-    const int n2 = col_of(o);
-    if (o != cur_o) {
-      cur_o = o;
-#pragma unroll
-      for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
-      base = tw_p<-1>(a.twp, (uint32_t)(n2 * lane));
-      tk[w][lane] = tw_p<-1>(a.twp, (uint32_t)(32 * n2 * lane));
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    double2 v[32];
-    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const double2 uv = Sw[lane + 32 * r];
-      const double x = uv.x * nl[r], y = uv.y * nl[r];
-      v[r] = make_double2(x, y);
-      const int64_t i = (int64_t)(lane + 32 * r) * kW_N2 + n2;  // zero-filled past m
-      if (i >= 1) {
-        const double sz = (double)(i + 1);
-        s0 += x;
-        s1 += sz * x;
-        s2 += y;
-        s3 += sz * y;
-      }
-    }
-#pragma unroll
-    for (int r = 16; r < 32; ++r) v[r] = czero();
-    __syncwarp();
-    if (item + 1 < it1) prefetch(item + 1);
-    // L2 bulk prefetch of the item after next: opt-in (AGK_DBG & 32768) since the tile store is
-    // interleaved with step A (measured 1.5-2 us faster without; the row pass keeps its prefetch)
-    if (item + AGK_PFDIST(a) + 1 < it1 && lane == 0 && AGK_XDBG(a, 32768)) {
-      const int o2 = (item + AGK_PFDIST(a) + 1) / gcount, ub2 = g0 + (item + AGK_PFDIST(a) + 1) % gcount;
-      prefetch_l2(a.uvg + ((int64_t)ub2 * kW_N2 + col_of(o2)) * kW_H, kW_H * sizeof(double2));
-    }
-    {
-      // the previous item's tile goes out while step A runs (one instruction stream, so the
-      // stores interleave with the transform); the first item has no previous tile (sti < it0)
-      const int sti = item - 1;
-      if constexpr (SV == 0) {
-        if (!AGK_XDBG(a, 4)) warp_fft1024_a<-1, true>(v, tw, lane);  // table twiddles (recurrence / 2-level measured slower)
-        if (sti >= it0 && !AGK_XDBG(a, 2)) store_tile(sti);
-      } else {
-        // step A in pieces with a quarter of the tile store after each
-        double2 ea[16], ob[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          ea[r] = v[r];
-          ob[r] = mul_w32<-1>(v[r], r);
-        }
-        store_quarter(sti, 0);
-        Dft<16, -1>::run(ea);
-        store_quarter(sti, 1);
-        Dft<16, -1>::run(ob);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          v[2 * k] = ea[k];
-          v[2 * k + 1] = ob[k];
-        }
-        store_quarter(sti, 2);
-        twiddle_a_rec<-1>(v, tw, lane);  // 5 shared loads instead of 31: the LSU is busy storing (-5 us)
-        store_quarter(sti, 3);
-      }
-      __syncthreads();  // every warp has read the tile: it is free for the exchanges
-      if (!AGK_XDBG(a, 8)) warp_fft1024_tb<-1>(v, T, w, lane);
-    }
-    // four-step twiddle W_P^{n2 k1c} = W_P^{n2 lane} W_P^{32 n2 k}, k1c = lane + 32 k
-    __syncwarp();
-    if (!AGK_XDBG(a, 2048)) {
-      // four chains t_{j+4m} = (base W_P^{32 n2 j}) (W_P^{128 n2})^m: 5 shared loads instead
-      // of 32 on the critical path, at most 7 roundings per factor
-      double2 t[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = cmul(base, tk[w][j]);
-      const double2 st = tk[w][4];
-#pragma unroll
-      for (int mm = 0; mm < 8; ++mm) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) T[tile_idx(lane + 32 * (4 * mm + j), w)] = cmul(v[4 * mm + j], t[j]);
-        if (mm < 7) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) t[j] = cmul(t[j], st);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) T[tile_idx(lane + 32 * k, w)] = cmul(v[k], cmul(base, tk[w][k]));
-    }
-    s0 = warp_sum(s0);
-    s1 = warp_sum(s1);
-    s2 = warp_sum(s2);
-    s3 = warp_sum(s3);
-    if (lane == 0) {
-      red[w][0] = s0;
-      red[w][1] = s1;
-      red[w][2] = s2;
-      red[w][3] = s3;
-    }
-    __syncthreads();
-    if (tid < 4) {
-      double t = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) t += red[q][tid];
-      a.partials[((int64_t)ub * a.nblk_colfwd + o) * 4 + tid] = t;
-    }
-  }
-  if (it0 < it1 && !AGK_XDBG(a, 2)) store_tile(it1 - 1);
-  tl_mark(a, 1, 2);
-}
-
-
-
-// Column pass with the transposition done by the transform's own exchange (no output tile):
-// step A as in k_colt (warp w = column w of the octet, lane = l), exchanged through the CTA's
+// Column pass: a CTA item is (column octet o, rank): the 8 columns n2 = 16 (o >> 1) + 2 c + (o & 1),
+// whose outputs are the 8 consecutive slots (o & 1) * 1024 + 8 (o >> 1) + c of every row (one
+// 128-byte line per row). Items are rank-minor, so n is reloaded only per octet. The operands
+// (U,V) of the next item are staged by cp.async while the current item is transformed.
+//
+// The transposition is done by the transform's own exchange (no output tile): step A per warp
+// (warp w = column w of the octet, lane = l: radix-32 DFT with the upper half zero as two radix-16
+// DFTs, twiddles by recurrence), exchanged through the CTA's
 // 1024 x 8 tile, but step B is dealt across the CTA by (column, k): lane (c = lane & 7,
 // kk = lane >> 3) of warp w' runs the radix-32 DFT over l of column c at k = 4 w' + kk and so
 // holds X_c[k + 32 q], q < 32. A warp store at fixed q is then 4 rows (k .. k+3... one per kk) of
 // 8 consecutive slots = four full 128-byte Y lines straight from registers: the tile write-back
 // (32 STS.128 + 32 LDS.128 per thread and item) and the wait for the tile to drain are gone.
-// Same arithmetic per element as k_colt (bitwise the same Y).
 __global__ void __launch_bounds__(256, 1) k_colx(RhsArgs a, int g0, int gcount) {
   tl_mark(a, 1, 0);
   extern __shared__ double2 smem[];
@@ -334,7 +162,7 @@ __global__ void __launch_bounds__(256, 1) k_colx(RhsArgs a, int g0, int gcount) 
 #pragma unroll
       for (int r = 0; r < 16; ++r) nl[r] = a.ng[(int64_t)n2 * kW_H + lane + 32 * r];
       // four-step factors of the step-B role: W_P^{n2B k1}, k1 = kB + 32 q, as four chains
-      // t_{j+4m} = (W_P^{n2B kB} W_P^{32 n2B j}) (W_P^{128 n2B})^m (the factors k_colt forms)
+      // t_{j+4m} = (W_P^{n2B kB} W_P^{32 n2B j}) (W_P^{128 n2B})^m 
       const int n2B = col_of(o, cB);
       const double2 base = tw_p<-1>(a.twp, (uint32_t)(n2B * kB));
 #pragma unroll
@@ -411,7 +239,11 @@ __global__ void __launch_bounds__(256, 1) k_colx(RhsArgs a, int g0, int gcount) 
 #pragma unroll
     for (int mm = 0; mm < 8; ++mm) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) yq[(int64_t)(4 * mm + j) * 32 * kW_YS] = cmul(v[4 * mm + j], t[j]);
+      for (int j = 0; j < 4; ++j) {
+        const double2 yv = cmul(v[4 * mm + j], t[j]);
+        double2* dst = yq + (int64_t)(4 * mm + j) * 32 * kW_YS;
+        *dst = yv;
+      }
       if (mm < 7) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) t[j] = cmul(t[j], stB);
@@ -429,6 +261,12 @@ __global__ void __launch_bounds__(256, 1) k_colx(RhsArgs a, int g0, int gcount) 
 // LAST (the launch of the last rank group): the half then runs the inverse row transform of its
 // accumulated Hermitian row k1 (2 warps, radix-2 DIF + 1024-point inverse FFTs) and the inverse
 // four-step twiddle, writing G in place of the accumulator row.
+// The shared-memory traffic of a transform is spread through its arithmetic instead of issued in
+// bursts: the exchange stores follow each step-A twiddle product, and the results are parked where
+// the thread itself read its step-B inputs (xs[lane * 33 + k] holds X[lane + 32 k]: no warp barrier
+// between step B and the park; the product phase reads bin q at (q & 31) * 33 + (q >> 5),
+// conflict-free since consecutive lanes are 33 entries apart); rank weights are staged in shared
+// memory once per CTA (row pass 180 -> 174 us at config 4).
 // Launched with 2 row pairs per half (grid = ceil(513 / 4) = 129 CTAs at N1 = 1024) so the SMs
 // left over run the non-birth part D concurrently (k_dvec, programmatic dependent launch).
 // The row kernel tests its experiment bits at run time (a.dbg is 0 unless an AGK_EXPERIMENTS
@@ -443,7 +281,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
   double2* tw = X + 8 * kXR;       // W_1024^{l k1}, [k1][l]
   double2* twh = tw + 1024;        // W_2048^j, j < 1024
   __shared__ double2 tkk[8][32];
-  // after the column pass completed: k_dvec (dependent) reads its moment partials
+  __shared__ double wq_s[32];
   tl_mark_rt(a, 2, 0);
   pdl_entry();
   tl_mark_rt(a, 2, 1);
@@ -457,6 +295,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     tw[i] = __ldg(a.tw32 + i);
     twh[i] = __ldg(a.tw2048h + i);
   }
+  if (tid < 32 && tid < gcount) wq_s[tid] = 0.25 * a.uniq_weight[g0 + tid];
   __syncthreads();
   double2* Xh = X + hf * 4 * kXR;
   double2* Xw = X + w * kXR;
@@ -466,20 +305,11 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     double2 acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = first ? czero() : a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j];
-    // rank g's samples are loaded while rank g-1's split product runs (v is free once the
-    // transform has been parked in Xw), so the HBM latency hides behind the product phase
     double2 v[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) v[r] = rsrc[lane + 32 * r];
-    // the radix-2 twiddles of this thread's bins, the same for every rank: W_2048^q' for q' = ht +
-    // 128 j (row k1) and, with the combination's sign folded in, -W_2048^-m' for the partner bins
-    // of row N1-k1 (m' = 1023 - q', or N2 - q for row 0, whose bin 0 pairs with itself unrotated)
-    // (hoisted into registers for the last launch; the accumulating launches of a multi-group
-    // plan, which also carry the accumulator through global memory, form them per rank instead,
-    // where the 32 extra live registers would spill)
     double2 tw1[8], tw2[8];
     const double2 wb1 = twh[ht];
-    // W_2048^(1024 - ht) (row 0) or W_2048^(1023 - ht) = -conj(W_2048^(ht + 1)), negated
     const double2 wb2 = k1 == 0 ? make_double2(wb1.x, -wb1.y) : make_double2(twh[ht + 1].x, -twh[ht + 1].y);
     auto tw_of = [&](int j, double2& t1w, double2& t2w) {
       t1w = mul_w16<-1>(wb1, j);
@@ -489,11 +319,15 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 #pragma unroll
       for (int j = 0; j < 8; ++j) tw_of(j, tw1[j], tw2[j]);
     }
+    // parked bin q of a region: (q & 31) * 33 + (q >> 5). This thread's bins q' = ht + 128 j and
+    // their partners m = 1023 - q' (row 0: (1024 - q') & 1023) are 4 entries apart per j.
+    const int pl = ht & 31, pc = ht >> 5;
+    const double2* pq = Xh + pl * 33 + pc;
+    const double2* pm = Xh + 2 * kXR + (k1 != 0 ? (31 - pl) * 33 + 31 - pc : (pl ? (32 - pl) * 33 + 31 - pc : 32 - pc));
+    const double2* pm0 = (k1 == 0 && ht == 0) ? Xh + 2 * kXR : pm;
     for (int g = 0; g < gcount; ++g) {
-      const double wq = 0.25 * a.uniq_weight[g0 + g];
+      const double wq = gcount <= 32 ? wq_s[g] : 0.25 * a.uniq_weight[g0 + g];
       if (lane == 0 && !ROW_XDBG(a, 128)) {
-        // the 16 KB of the item pfd steps ahead (the next row pair's ranks after the last) into
-        // L2, so the register loads of the next items hit L2
         int gn = g + AGK_PFDIST(a), k1n = k1;
         if (gn >= gcount) {
           gn -= gcount;
@@ -504,10 +338,17 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           prefetch_l2(a.y + (int64_t)gn * kW_YP + (int64_t)rown * kW_YS + h * (kW_N2 / 2), 1024 * sizeof(double2));
         }
       }
-      if (!ROW_XDBG(a, 16)) warp_fft1024<-1, false, true>(v, Xw, tw, lane);  // step-A twiddles by recurrence (table: same time)
-      __syncwarp();
+      if (!ROW_XDBG(a, 16)) {
+        Dft<32, -1>::run(v);
+        twiddle_a_rec_store<-1>(v, tw, lane, [&](int k, double2 x) { Xw[k * 33 + lane] = x; });
+        __syncwarp();
 #pragma unroll
-      for (int k = 0; k < 32; ++k) Xw[lane + 32 * k] = v[k];
+        for (int l = 0; l < 32; ++l) v[l] = Xw[lane * 33 + l];
+        Dft<32, -1>::run(v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) Xw[lane * 33 + k] = v[k];
+      }
+      __syncwarp();  // keeps the next rank's loads (32 live registers) behind the transform
       if (g + 1 < gcount && !ROW_XDBG(a, 64)) {
         const double2* __restrict__ src = rsrc + (int64_t)(g + 1) * kW_YP;
 #pragma unroll
@@ -517,11 +358,10 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
       if (!ROW_XDBG(a, 32))
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int qp = ht + 128 * j;
-        // partner bins of q' and q' + 1024 in row N1-k1 (row 0 pairs with itself at N2 - q)
-        const int m = (k1 == 0) ? ((kW_N1 - qp) & (kW_N1 - 1)) : (kW_N1 - 1 - qp);
-        const double2 e1 = Xh[qp], o1 = Xh[kXR + qp];
-        const double2 e2 = Xh[2 * kXR + m], o2 = Xh[3 * kXR + m];
+        // bin q' = ht + 128 j sits at pq[4 j]; its partner bin at pm[-4 j] (pm0: row 0's bin 0)
+        const double2 e1 = pq[4 * j], o1 = pq[kXR + 4 * j];
+        const double2* pmj = j == 0 ? pm0 : pm;
+        const double2 e2 = pmj[-4 * j], o2 = pmj[kXR - 4 * j];
         double2 t1w, t2w;
         if constexpr (LAST) {
           t1w = tw1[j];
@@ -541,7 +381,6 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
 #pragma unroll
       for (int j = 0; j < 16; ++j) a.acc[(int64_t)k1 * kW_N2 + ht + 128 * j] = acc[j];
     } else {
-      // inverse row transform of the accumulated row k1 (rho = 0 warps; regions 2, 3 hold the row)
       double2* Ar = Xh + 2 * kXR;  // 2120 >= 2048 contiguous entries
 #pragma unroll
       for (int j = 0; j < 16; ++j) Ar[ht + 128 * j] = acc[j];
@@ -554,7 +393,6 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
           v[r] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), cconj(twh[lane + 32 * r]));
         }
         warp_fft1024<+1, false>(v, Xw, tw, lane);
-        // T[c2], c2 = 2(lane + 32k) + h; G = T W_P^{-c2 k1} = T W_P^{-(2 lane + h) k1} W_P^{-64 k1 k}
         const double2 base = tw_p<+1>(a.twp, (uint32_t)((2 * lane + h) * k1));
         tkk[w][lane] = tw_p<+1>(a.twp, (uint32_t)((64 * k1 * lane) & (P - 1)));
         __syncwarp();
@@ -759,8 +597,7 @@ __global__ void __launch_bounds__(kCW * 32, kCW == 8 ? 1 : 2) k_colinvw(RhsArgs 
   tl_mark(a, 4, 2);
 }
 
-static size_t smem_colt() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024) * sizeof(double2); }
-static size_t smem_colx() { return smem_colt() + (size_t)4 * 256 * sizeof(double2); }
+static size_t smem_colx() { return (size_t)(8 * kW_N1 + 8 * kW_H + 1024 + 4 * 256) * sizeof(double2); }
 static size_t smem_rowd() { return (size_t)(8 * kXR + 2048) * sizeof(double2); }
 template <int CW>
 static size_t smem_colinvw_t() {
@@ -778,8 +615,6 @@ cudaError_t rhs_w_set_smem_limits() {
   cudaError_t e;
 #define SET(fn, bytes) \
   if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes))) != cudaSuccess) return e;
-  SET(k_colt<0>, smem_colt());
-  SET(k_colt<1>, smem_colt());
   SET(k_colx, smem_colx());
   SET(k_rowd<false>, smem_rowd());
   SET(k_rowd<true>, smem_rowd());
@@ -818,14 +653,7 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
     const bool last = g0 + gc >= a.rf;
     const int items = (kW_N2 / 8) * gc;
     const int cgrid = items < nsm ? items : nsm;
-    static const int stv = knob("AGK_STV", 2);  // 2: transposing step B; 1: tile write-back in quarters
-    if (stv == 2) {
-      AGK_CK(launch_k(k_colx, cgrid, 256, smem_colx(), s, pdl && (pdl_mask() & 2), a, g0, gc));
-    } else if (stv == 1) {
-      AGK_CK(launch_k(k_colt<1>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
-    } else {
-      AGK_CK(launch_k(k_colt<0>, cgrid, 256, smem_colt(), s, pdl && (pdl_mask() & 2), a, g0, gc));
-    }
+    AGK_CK(launch_k(k_colx, cgrid, 256, smem_colx(), s, pdl && (pdl_mask() & 2), a, g0, gc));
     if (mark) mark(mk, K_COL_FWD, s);
     if (!last) {
       AGK_CK(launch_k(k_rowd<false>, rgrid, 256, smem_rowd(), s, pdl, a, g0, gc, (int)(g0 == 0)));

@@ -25,7 +25,7 @@ METRICS = [
     "launch__grid_size",
     "launch__block_size",
 ]
-CLASS = {"k_colt": "col_fwd", "k_rowd": "row", "k_dvec": "dvec", "k_colinvw": "col_inv",
+CLASS = {"k_colx": "col_fwd", "k_colt": "col_fwd", "k_rowd": "row", "k_dvec": "dvec", "k_colinvw": "col_inv",
          "k_transpose_n": "transpose", "k_scalars_w": "scalars"}
 
 
