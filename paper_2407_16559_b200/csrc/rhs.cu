@@ -535,11 +535,13 @@ bool pdl_enabled() {
   return on;
 }
 int pdl_mask() {
-  // measured per edge (tools/ab.sh): on for the transpose -> column pass, -> inverse column
-  // pass and the RK-trial chain, and for the four-step path (P = 2^13, and the mid sizes, whose
-  // kernels trigger their dependents at their end: -0.5 us at configs 2 and 3; triggered at entry
-  // the early-placed dependent grid was slower); off for the column -> row passes
-  static const int m = knob("AGK_PDLMASK", 2 | 8 | 16 | 32 | 64);
+  // measured per edge (tools/gpu/pdl.sh, profiles/pdl_r02i.txt): on for the inverse column pass (8),
+  // the RK-trial chain (16) and the four-step path (32: P = 2^13; 64: the mid sizes, whose kernels
+  // trigger their dependents at their end: -0.5 us at configs 2 and 3; triggered at entry the
+  // early-placed dependent grid was slower); off for the transpose (1), for the column pass as the
+  // transpose's dependent (2: with k_colx its early-placed CTAs cost 3.7 us per RHS at config 4 and
+  // 6 us at config 5) and for the column -> row edge (4)
+  static const int m = knob("AGK_PDLMASK", 8 | 16 | 32 | 64);
   return m;
 }
 
