@@ -10,6 +10,10 @@ Run here (where /root/reference exists), one process per case (they are single-t
 
     python tests/golden/make_parity_runs.py --list
     python tests/golden/make_parity_runs.py CASE [--floor port_fma]
+    python tests/golden/make_parity_runs.py CASE --which floor --floor port_pad2 --leg floor2
+
+(a second floor build, the restatement with a 2x-padded FFT, i.e. a different FFT roundoff pattern:
+the floor of a case is the larger of its floor legs)
 
 Writes tests/golden/parity/CASE__ref.npz and CASE__floor.npz. The state is stored compactly: the head of the final state
 up to the last index with n_s > 1e-13 max n (everything that can move the normwise or element-wise
@@ -111,23 +115,62 @@ def run_one(which, name):
     return s
 
 
+def fluctuation(name, frac=0.01, nsnap=40):
+    """How much the REFERENCE's own trajectory moves about its final state: the reference is
+    restarted from its golden final state (the system is autonomous) and run a further `frac` of
+    the horizon with every step recorded and `nsnap` snapshots. At a steady state held at the
+    controller's stability limit, N(t) and n_s(t) wander step to step by far more than 1e-8 (config 5
+    at M = 4096 with RK2: 8e-5 in N), so where a run ends inside that band is decided by roundoff:
+    a final value cannot be pinned tighter than this band. Written to CASE__fluct.npz."""
+    z = np.load(os.path.join(OUT, f"{name}__ref.npz"))
+    cfg, m, st, t_end = CASES[name]
+    x0 = np.zeros(m)
+    head = np.asarray(z["head"], dtype=np.float64)
+    x0[: head.size] = head
+    if "sample_idx" in z.files:
+        x0[np.asarray(z["sample_idx"])] = np.asarray(z["sample_val"])
+    md, _, ctl, _ = case_inputs(name)
+    dt = frac * t_end
+    snaps = np.linspace(dt / nsnap, dt, nsnap)
+    r = O.Oracle("reference").run(md, x0, ctl, dt, snapshot_times=snaps, record=O.RECORD_EVERY_STEP,
+                                  records_capacity=4000000)
+    k = np.arange(1, m + 1, dtype=np.float64)
+    n0, m10, mx = x0.sum(), float(np.dot(k, x0)), float(np.max(np.abs(x0)))
+    N = np.array([q["density"] for q in r["records"]])
+    M1 = np.array([q["mass"] for q in r["records"]])
+    S = np.asarray(r["snapshots"])
+    big = x0 > 1e-9 * mx
+    out = dict(N=float(np.max(np.abs(N - n0)) / abs(n0)), M1=float(np.max(np.abs(M1 - m10)) / abs(m10)),
+               state=float(np.max(np.abs(S - x0)) / mx),
+               elem=float(np.max(np.abs(S[:, big] / x0[big] - 1.0))) if big.any() else 0.0,
+               window=dt, steps=int(r["total_accepted"]), rejects=int(r["total_rejects"]))
+    print(name, "fluct", out, flush=True)
+    np.savez_compressed(os.path.join(OUT, f"{name}__fluct.npz"), **{k2: np.asarray(v) for k2, v in out.items()})
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("case", nargs="?")
     ap.add_argument("--list", action="store_true")
     ap.add_argument("--floor", default="port_fma", help="second CPU build for the noise floor ('' = none)")
     ap.add_argument("--which", default="both", choices=["both", "ref", "floor"])
+    ap.add_argument("--fluct", action="store_true",
+                    help="write CASE__fluct.npz: the reference trajectory's own fluctuation about its final state")
+    ap.add_argument("--leg", default="floor", help="file suffix of the floor leg (floor, floor2: a second floor build)")
     a = ap.parse_args()
     if a.list or not a.case:
         print("\n".join(CASES))
         return
     os.makedirs(OUT, exist_ok=True)
     cfg, m, st, t_end = CASES[a.case]
+    if a.fluct:
+        fluctuation(a.case)
+        return
     legs = []
     if a.which in ("both", "ref"):
         legs.append(("ref", "reference"))
     if a.which in ("both", "floor") and a.floor:
-        legs.append(("floor", a.floor))
+        legs.append((a.leg, a.floor))
     for key, which in legs:
         s = run_one(which, a.case)
         out = dict(config=np.array(cfg), m=np.array(m), stepper=np.array(st), t_end=np.array(t_end),

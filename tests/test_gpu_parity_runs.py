@@ -15,6 +15,13 @@ trajectory cannot be held tighter than that floor, so a bar is raised to 10x the
 10x the floor exceeds it (the floor is ONE sample of the build-to-build spread; the device's
 distance is another), and the raised bars are listed. Every measured distance, floor and bar is
 appended to $AGK_PARITY_REPORT (JSON lines) when set (-> profiles/parity_r02.json).
+
+Steady states held at the step controller's stability limit (config 5 at M = 4096 to t = 1e5: a
+quarter of all trials are rejected) wander step to step: along the reference's OWN trajectory N(t)
+moves by 1.5e-5 (RK2) within the last 1 % of the horizon. Those cases carry CASE__fluct.npz (the
+reference restarted from its final state, make_parity_runs.py --fluct) and no final value is held
+tighter than that band; test_restart_window shows the device and the reference in step through
+such a window when both start from the same state.
 """
 import glob
 import json
@@ -118,14 +125,22 @@ def test_parity_run(agk, name):
     g = summarize_state(rep.final_state)
     g["accepted"] = rep.total_accepted
     mg = distance(g, want)
-    mf = distance(floor_run, want) if floor_run is not None else {k: 0.0 for k in BARS}
-    bars = {k: max(b, FLOOR_FACTOR * mf[k]) for k, b in BARS.items()}
+    floors = [f for f in (floor_run, load(name, "floor2")) if f is not None]
+    mfs = [distance(f, want) for f in floors]
+    mf = {k: max([x[k] for x in mfs], default=0.0) for k in BARS}
+    # the reference trajectory's own wander about its final state (CASE__fluct.npz, where made: the
+    # steady states held at the controller's stability limit): where a run ends inside that band is
+    # decided by roundoff, so no final value is held tighter than the band
+    fl = load(name, "fluct")
+    band = {k: (float(fl[k]) if fl is not None and k in fl else 0.0) for k in BARS}
+    bars = {k: max(b, FLOOR_FACTOR * mf[k], band[k]) for k, b in BARS.items()}
     path = os.environ.get("AGK_PARITY_REPORT")
     if path:
         with open(path, "a") as f:
             f.write(json.dumps(dict(case=name, config=cfg, m=m, scheme=st, t_end=t_end, gpu=mg, cpu_floor=mf,
-                                    floor_build=str(floor_run["build"]) if floor_run is not None else None,
+                                    floor_build="+".join(str(f["build"]) for f in floors) or None,
                                     bars=bars, raised=[k for k in BARS if bars[k] != BARS[k]],
+                                    ref_fluctuation_band=band if fl is not None else None,
                                     gpu_counts=dict(accepted=rep.total_accepted, rejects=rep.total_rejects,
                                                     rhs_evals=rep.total_rhs_evals, wall_s=rep.wall_seconds),
                                     ref_counts=dict(accepted=int(want["accepted"]), rejects=int(want["rejects"]),
@@ -133,3 +148,33 @@ def test_parity_run(agk, name):
                                                     cpu_wall_s=float(want["wall_s"])))) + "\n")
     for k in BARS:
         assert mg[k] <= bars[k], (name, k, mg[k], bars[k], mf[k])
+
+
+@pytest.mark.parametrize("name,t0,dt", [("c5_m4096_rk2", 99000.0, 1000.0), ("c5_m4096_rkf45", 99000.0, 1000.0)])
+def test_restart_window(agk, name, t0, dt):
+    """From the device's own state at t0 (deep in the steady state at the stability limit), the
+    device and the oracle (pinned bitwise to the reference) integrate the same further window:
+    started from the same state they must agree to the north_star bars (simulator.cpp:170-217)."""
+    from oracle import oracle as O
+    cfg, m, st, _ = CASES[name]
+    kind, variant, sources, lam, init, tol = CONFIG[cfg]
+    u, v = factors("brownian2", m)
+    ws = agk.RhsWorkspace(agk.Model(u, v, variant, list(sources), lam))
+    ctl = agk.StepControl(stepper=STEPPERS[st], tol=tol)
+    x0 = np.array(agk.run(ws, agk.SimulationConfig(ctl, t0, np.zeros(m))).final_state)
+    rg = agk.run(ws, agk.SimulationConfig(ctl, dt, x0))
+    ws.close()
+    ro = O.Oracle("port").run(O.Model(u, v, variant, list(sources), lam), x0,
+                              O.Control(stepper=STEPPERS[st], mode=O.ADAPTIVE, tol=tol), dt)
+    fg, fo = np.array(rg.final_state), np.array(ro["final_state"])
+    k = np.arange(1, m + 1, dtype=np.float64)
+    d = dict(N=abs(fg.sum() - fo.sum()) / fo.sum(), M1=abs(np.dot(k, fg) - np.dot(k, fo)) / np.dot(k, fo),
+             state=float(np.max(np.abs(fg - fo)) / np.max(np.abs(fo))),
+             accepted=abs(rg.total_accepted - ro["total_accepted"]) / ro["total_accepted"])
+    path = os.environ.get("AGK_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(dict(case=f"{name}_restart_t{t0:g}+{dt:g}", restart=d,
+                                    gpu_counts=dict(accepted=rg.total_accepted, rejects=rg.total_rejects),
+                                    ref_counts=dict(accepted=ro["total_accepted"], rejects=ro["total_rejects"]))) + "\n")
+    assert d["N"] <= 1e-8 and d["M1"] <= 1e-8 and d["state"] <= 1e-6 and d["accepted"] <= 0.02, d
