@@ -31,8 +31,8 @@ for r in out["runs"]:
     print(f"| {r['case']} | {r['gpu_counts']['accepted']} / {r['ref_counts']['accepted']} | {cell('N')} | {cell('M1')} "
           f"| {cell('state')} | {cell('elem')} | {g['accepted']:.1e} | {raised} |")
 print()
-print("| restart window (device and oracle from the same device state) | accepted GPU / ref | N | M1 | n_s normwise |")
-print("|---|---|---|---|---|")
+print("| restart window (device and oracle from the same device state) | accepted GPU / ref | N | M1 | n_s normwise | records in lock-step |")
+print("|---|---|---|---|---|---|")
 for r in out["restart_windows"]:
     d = r["restart"]
-    print(f"| {r['case']} | {r['gpu_counts']['accepted']} / {r['ref_counts']['accepted']} | {d['N']:.1e} | {d['M1']:.1e} | {d['state']:.1e} |")
+    print(f"| {r['case']} | {r['gpu_counts']['accepted']} / {r['ref_counts']['accepted']} | {d['N']:.1e} | {d['M1']:.1e} | {d['state']:.1e} | {d.get('lockstep_records', '')} |")
