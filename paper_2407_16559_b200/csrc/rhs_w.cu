@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(256, 1) k_rowd(RhsArgs a, int g0, int gcount, 
     const double2* pm = Xh + 2 * kXR + (k1 != 0 ? (31 - pl) * 33 + 31 - pc : (pl ? (32 - pl) * 33 + 31 - pc : 32 - pc));
     const double2* pm0 = (k1 == 0 && ht == 0) ? Xh + 2 * kXR : pm;
     for (int g = 0; g < gcount; ++g) {
-      const double wq = gcount <= 32 ? wq_s[g] : 0.25 * a.uniq_weight[g0 + g];
+      const double wq = wq_s[g];  // (the plan caps a group at 16 ranks)
       if (lane == 0 && !ROW_XDBG(a, 128)) {
         int gn = g + AGK_PFDIST(a), k1n = k1;
         if (gn >= gcount) {
