@@ -79,6 +79,7 @@ struct RhsArgs {
   double* dpair;
   double* dpart;
   int dbg;                 // experiment switches (AGK_DBG), 0 in production
+  unsigned long long* tl;  // timeline stamps (AGK_DBG & 512, experiments build), else null
 };
 
 // Launch geometry and per-handle tables for one problem size.
@@ -109,10 +110,12 @@ enum KernelClass { K_SMALL = 0, K_COL_FWD = 1, K_ROW = 2, K_COL_INV = 3, K_TRANS
 #ifdef AGK_EXPERIMENTS
 int knob(const char* name, int dflt);
 #define AGK_XDBG(a, bits) (((a).dbg & (bits)) != 0)
+#define AGK_TL(a, k, what) tl_stamp((a).tl, k, what)
 #define AGK_PFDIST(a) ((a).pfd)
 #else
 inline int knob(const char*, int dflt) { return dflt; }
 #define AGK_XDBG(a, bits) false
+#define AGK_TL(a, k, what) ((void)0)
 #define AGK_PFDIST(a) 1  // L2 prefetch distance of the row pass (items), measured best
 #endif
 bool pdl_enabled();
@@ -140,6 +143,16 @@ inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 #ifdef __CUDACC__
+// timeline stamp of kernel class k (0 first arrival, 1 first start of work, 2 last exit), %globaltimer ns
+__device__ __forceinline__ void tl_stamp(unsigned long long* tl, int k, int what) {
+  if (tl && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    if (what < 2) atomicMin(tl + 3 * k + what, t);
+    else atomicMax(tl + 3 * k + what, t);
+  }
+}
+unsigned long long* timeline_ptr();  // rhs_w.cu: device address of the timeline array
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_entry() {

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   const int tid = threadIdx.x, c = tid % C, j = tid / C;
   const int64_t n2 = (int64_t)blockIdx.x * C + c;
   const int64_t N2 = a.n2, m = a.m, P = (int64_t)N1 * N2;
+  AGK_TL(a, 1, 0);
   // stage this thread's U_a, V_a elements of unique rank ub (zero-filled past m)
   auto prefetch = [&](int ub) {
     const int ra = a.uniq_rank[ub];
@@ -208,6 +209,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
   load_twiddles<N1, E1>(smtw, a.tw_n1);
   const TwSeries<-1> tw0(a.twp, (uint32_t)(n2 * j), (uint32_t)(n2 * T1));  // four-step twiddles
   pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
+  AGK_TL(a, 1, 1);
   if (a.skip && *a.skip) {
     cp_async_wait_all();
     return;
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
       for (int q = 0; q < 4; ++q) a.partials[((int64_t)ub * a.nblk_colfwd + blockIdx.x) * 4 + q] = s[q];
     }
   }
+  AGK_TL(a, 1, 2);
   pdl_trigger();
 }
 
@@ -278,12 +281,14 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
   extern __shared__ double2 smem[];
   double2* smtw = smem + 2 * PL::SMEM;
   double2* stage = smtw + PL::TWS;  // [E2][NT]: this thread's elements of the next rank's row
+  AGK_TL(a, 2, 0);
   load_twiddles<N2, E2>(smtw, a.tw_n2);  // immutable table: overlaps the predecessor's tail
   const int tid = threadIdx.x, team = tid / T2, j = tid % T2;
   const int n1 = a.n1;
   const int k1 = blockIdx.x;
   const TwSeries<+1> itw0(a.twp, (uint32_t)(j * k1), (uint32_t)(T2 * k1));  // inverse four-step twiddles
   pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
+  AGK_TL(a, 2, 1);
   if (a.skip && *a.skip) return;
   const int row = team == 0 ? k1 : (n1 - k1) & (n1 - 1);
   const int64_t P = (int64_t)n1 * N2;
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
       a.acc[(int64_t)k1 * N2 + c2] = cmul(u[r], tw.next());
     }
   }
+  AGK_TL(a, 2, 2);
   pdl_trigger();
 }
 
@@ -376,8 +382,10 @@ __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
   constexpr int RG = PL::template smem<kNoPad>();
   extern __shared__ double2 smem[];
   double2* smtw = smem + CP * RG;
+  AGK_TL(a, 4, 0);
   load_twiddles<N1, E1>(smtw, a.tw_n1);  // immutable table: overlaps the predecessor's tail
   pdl_wait();  // dependents are triggered at the end (mid-size path: trigger late)
+  AGK_TL(a, 4, 1);
   if (a.skip && *a.skip) return;
   const int tid = threadIdx.x, c = tid % CP, j = tid / CP;
   const int64_t N2 = a.n2, m = a.m;
@@ -432,6 +440,7 @@ __global__ void __launch_bounds__(CP*(N1 / E1)) k_col_inv(RhsArgs a) {
     }
   }
   if (blockIdx.x == 0 && tid == 0) a.out[0] = epilogue0(a, n);
+  AGK_TL(a, 4, 2);
   pdl_trigger();
 }
 
@@ -567,6 +576,7 @@ template <typename CF>
 static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, Marks* mk) {
   RhsArgs first = a0;
   first.nblk_colfwd = CF::N2 / CF::C;
+  if (knob("AGK_DBG", 0) & 512) first.tl = timeline_ptr();  // experiments build only
   const RhsArgs a = rest_args(first);
   const size_t sm1 = CF::SM_COLFWD, sm2 = CF::SM_ROW, sm3 = CF::SM_COLINV;
   const bool pdl = !mk && pdl_enabled() && (pdl_mask() & (CF::N1 * CF::N2 <= 8192 ? 64 : 32));

@@ -688,6 +688,12 @@ cudaError_t rhs_w_launch(const RhsPlan& p, const RhsArgs& a0, cudaStream_t s, vo
   return cudaGetLastError();
 }
 
+unsigned long long* timeline_ptr() {
+  static unsigned long long* p = nullptr;
+  if (!p) cudaGetSymbolAddress(reinterpret_cast<void**>(&p), g_timeline);
+  return p;
+}
+
 }  // namespace agk
 
 // diagnostics only (tools/timeline.py): reset (reset != 0) or read the AGK_DBG & 512 timeline
