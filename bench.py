@@ -369,6 +369,10 @@ def run_b200(args, world, rank, local):
                  "alg_flops_per_launch": dd["flops"] / dd["launches"],
                  "peak_source": "DFMA microbenchmark, profiles/probe_r01.txt"},
         "per_class_ms": {c: by_cls[c]["ms"] for c in by_cls},
+        "per_class": {c: {"ms": d["ms"], "alg_bytes": d["bytes"], "gbs": d["bytes"] / (d["ms"] * 1e-3) / 1e9,
+                          "hbm_frac": d["bytes"] / (d["ms"] * 1e-3) / 1e9 / hbm_peak,
+                          "fp64_frac": d["flops"] / (d["ms"] * 1e-3) / 1e12 / fp64_peak}
+                      for c, d in by_cls.items() if d["ms"] > 0},
         "whole_rhs": {"bytes_alg_survey": b_alg, "bytes_compulsory": b_comp, "flops_alg": survey_flops(M, rf),
                       "gbs_survey_model": b_alg / per_rhs_s / 1e9,
                       "frac_survey_model": b_alg / per_rhs_s / 1e9 / hbm_peak,

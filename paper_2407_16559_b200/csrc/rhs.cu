@@ -255,8 +255,12 @@ __global__ void __launch_bounds__(C*(N1 / E1)) k_col_fwd(RhsArgs a, int g0, int 
     if (g + 1 < gcount) prefetch(ub + 1);  // overlaps this rank's transforms
 #pragma unroll
     for (int r = H; r < E1; ++r) v[r] = czero();
+    AGK_TL(a, 5, 0);
+    AGK_TL(a, 5, 2);
     __syncthreads();  // twiddle tables ready / previous rank's smem reads done
     block_fft<N1, E1, -1, true, kNoPad>(v, sm, j, smtw);
+    AGK_TL(a, 5, 1);
+    AGK_TL(a, 6, 2);
     double2* __restrict__ yg = a.y + (int64_t)g * P;
     TwSeries<-1> tw = tw0;
 #pragma unroll
@@ -323,6 +327,7 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
       cp_async_wait_all();
 #pragma unroll
       for (int r = 0; r < E2; ++r) v[r] = stage[r * NT + tid];
+      AGK_TL(a, 7, 0);
       if (g + 1 < gcount) prefetch(g + 1);
     } else {
       const double2* __restrict__ yr = a.y + (int64_t)g * P + (int64_t)row * N2;
@@ -345,6 +350,8 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
       acc[q].y += wt * pr.y;
     }
   }
+  AGK_TL(a, 7, 1);
+  AGK_TL(a, 7, 2);
   if (!last) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) a.acc[(int64_t)k1 * N2 + tid + q * NT] = acc[q];
@@ -363,6 +370,7 @@ __global__ void __launch_bounds__(2 * (N2 / E2), MINB) k_row(RhsArgs a, int g0, 
   }
   __syncthreads();
   block_fft<N2, E2, +1, false>(u, smem, j, smtw, act);
+  AGK_TL(a, 6, 0);
   if (act) {
     TwSeries<+1> tw = itw0;
 #pragma unroll

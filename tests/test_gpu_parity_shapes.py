@@ -7,7 +7,8 @@ Cases ("Next round" item 1):
   * config 5 shape: M = 2^20, Brownian + 2 (R = 3 -> R_f = 2) with the monomer source;
   * config 4 shape: M = 2^20, R = 16 random kernel (std::mt19937_64 inputs), straight vs _ref;
   * the P = 2^21 warp path away from m = 2^20: odd m = 700001 and m = 2^20 - 3, both with
-    R_f = 2 (k_dvec after the row pass) and with R_f = 16 (k_dvec beside it);
+    R_f = 2 (k_dvec after the row pass) and with R_f = 16 (k_dvec beside it); R_f = 20 (two rank
+    groups: the accumulating row launch);
   * the m in (2^20, 2^22] four-step paths (P = 2^22, 2^23): m = 2^20 + 1, 3 * 2^20, 2^22;
   * one RKF45 `advance` (the device trial loop + controller) at config 5 full shape.
 Bar: north_star's 1e-11 max normwise relative error per RHS, exact zeros where the reference
@@ -103,6 +104,15 @@ def test_warp_path_odd_sizes(agk, ref, m):
     check(f"warp_m{m}_rf2", agk, ref, u, v, O.SOURCES, [(1, 1.0), (7, 0.5)], 0.0, cfg5_state(m, rng), want_rf=2)
     U, V, n = config4_inputs(m, 16)
     check(f"warp_m{m}_rf16_shatter", agk, ref, U, V, O.SHATTERING, [], 0.01, n, want_rf=16)
+
+
+def test_warp_path_two_rank_groups(agk, ref):
+    """More unique ranks than one warp-path group holds (16): R_f = 20 -> groups of 16 + 4, i.e. the
+    accumulating row launch (the Hermitian accumulator carried through global memory) followed by
+    the closing one (rhs.cpp:126-149 summed over all ranks)."""
+    m = 600001
+    U, V, n = config4_inputs(m, 20)
+    check("warp_m600001_rf20_two_groups", agk, ref, U, V, O.AGGREGATION, [], 0.0, n, want_rf=20)
 
 
 @pytest.mark.parametrize("m", [(1 << 20) + 1, 3 << 20, 1 << 22])

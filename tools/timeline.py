@@ -17,7 +17,10 @@ n = cfg["n0"] if cfg.get("tol") is None else np.random.default_rng(0).random(m) 
 nd = torch.from_numpy(np.ascontiguousarray(n)).cuda(); od = torch.empty_like(nd)
 lib = agk.load_library()
 buf = (ctypes.c_ulonglong * 24)()
-names = ["transpose", "col_fwd", "row", "dvec", "col_inv", "dvec(D done)"]
+names = ["transpose", "col_fwd", "row", "dvec", "col_inv", "dvec(D done)", "aux6", "aux7"]
+# mid sizes (four-step kernels): slot 5 = column pass [first CTA scaled its operands | first CTA past its FFT |
+# last CTA scaled its operands]; slot 6 = [first row CTA past its inverse FFT | - | last column CTA past its FFT];
+# slot 7 = row pass [first CTA has its samples | first CTA past forward FFT + product | last CTA past them]
 agk.eval_rhs_timed(ws, nd, od, 5)
 for rep in range(3):
     lib.agk_dbg_timeline(buf, 1)
@@ -25,8 +28,8 @@ for rep in range(3):
     lib.agk_dbg_timeline(buf, 0)
     t = [[int(buf[3 * k + i]) for i in range(3)] for k in range(8)]
     NONE = (0, 2**64 - 1)
-    t0 = min(t[k][0] for k in range(6) if t[k][0] not in NONE)
+    t0 = min(t[k][0] for k in range(5) if t[k][0] not in NONE)
     print(f"rep {rep}: graph {1e3 * ms:.1f} us")
-    for k in range(6):
+    for k in range(8):
         f = lambda x: "    -  " if x in NONE else f"{(x - t0) / 1e3:7.1f}"
         print(f"  {names[k]:14s} arrive {f(t[k][0])}  start {f(t[k][1])}  end {f(t[k][2])}")
