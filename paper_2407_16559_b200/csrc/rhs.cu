@@ -152,11 +152,17 @@ __global__ void __launch_bounds__(SmallCfg<P>::NT) k_small(RhsArgs a) {
 
 // ------------------------------------------------------------------ four-step path
 
-// Defaults: 4 points per thread up to P = 2^20 (latency-bound sizes want more warps; measured
-// 2x faster than 16 at P = 2^17, 2^18), 16 above.
-template <int L, int E1_ = (L <= 20 ? 4 : 16), int E2_ = (L <= 20 ? 4 : 16),
-          int C_ = (L <= 20 ? 4 : (L <= 21 ? 8 : 2)), int ROWMODE_ = 0>
+// Defaults (points per thread of the forward column, row and inverse column passes), measured per
+// size (tools/gpu/mvar.sh, profiles/mvar_r02u.txt): 4 up to P = 2^16 (the latency-bound small sizes
+// want more warps); 8 for the forward column and row passes at 2^17 <= P <= 2^20, whose 4-point
+// transforms were bound by shared-memory traffic (five exchange passes per 512-point transform:
+// 2.8 us of a 5 us phase, tools/timeline.py), with the inverse column pass at 2 (P = 2^17) or 4
+// points (its epilogue wants the threads); 16 above.
+template <int L, int E1_ = (L <= 16 ? 4 : (L <= 20 ? 8 : 16)), int E2_ = (L <= 16 ? 4 : (L <= 20 ? 8 : 16)),
+          int C_ = (L <= 20 ? 4 : (L <= 21 ? 8 : 2)), int ROWMODE_ = 0,
+          int E1I_ = (L <= 16 ? 4 : (L == 17 ? 2 : (L <= 20 ? 4 : E1_)))>
 struct Cfg {
+  static constexpr int E1I = E1I_;  // points per thread of the inverse column pass (its own choice)
   static constexpr int ROWMODE = ROWMODE_;  // 1: no staging, 2 CTAs/SM register budget
   static constexpr int N1 = 1 << (L / 2), N2 = 1 << (L - L / 2);
   static constexpr int E1 = E1_;
@@ -166,13 +172,15 @@ struct Cfg {
   static constexpr int T1 = N1 / E1, T2 = N2 / E2;
   using PL1 = FftPlan<N1, E1>;
   using PL2 = FftPlan<N2, E2>;
+  using PL1I = FftPlan<N1, E1I>;
   static constexpr int R1 = PL1::template smem<kNoPad>();  // column team region (no padding)
+  static constexpr int R1I = PL1I::template smem<kNoPad>();
   // + staging of the next rank's U, V (column kernel) / Y rows (row kernel)
   static constexpr size_t SM_COLFWD = (size_t)(C * R1 + PL1::TWS) * sizeof(double2) + (size_t)C * N1 * sizeof(double);
   static constexpr bool ROW_STAGE = ROWMODE == 0 && (2 * PL2::SMEM + PL2::TWS + 2 * N2) * 16 <= 232448;
   static constexpr int ROW_MINB = ROWMODE == 1 ? 2 : 1;
   static constexpr size_t SM_ROW = (size_t)(2 * PL2::SMEM + PL2::TWS + (ROW_STAGE ? 2 * N2 : 0)) * sizeof(double2);
-  static constexpr size_t SM_COLINV = (size_t)(CP * R1 + PL1::TWS) * sizeof(double2);
+  static constexpr size_t SM_COLINV = (size_t)(CP * R1I + PL1I::TWS) * sizeof(double2);
   static_assert(SM_COLFWD <= 232448 && SM_ROW <= 232448 && SM_COLINV <= 232448, "shared memory budget");
   static_assert(C * T1 >= 32 && 2 * T2 >= 32, "column-forward and row CTAs need full warps");
 };
@@ -598,7 +606,7 @@ static cudaError_t launch_four_step_cf(const RhsPlan& p, const RhsArgs& a0, cuda
                     gc, (int)(g0 == 0), (int)(g0 + gc >= a.rf)));
     mark(mk, K_ROW, s);
   }
-  AGK_CK(launch_k(k_col_inv<CF::N1, CF::E1, CF::CP>, CF::N2 / (2 * CF::CP), CF::CP * CF::T1, sm3, s, pdl, a));
+  AGK_CK(launch_k(k_col_inv<CF::N1, CF::E1I, CF::CP>, CF::N2 / (2 * CF::CP), CF::CP * (CF::N1 / CF::E1I), sm3, s, pdl, a));
   mark(mk, K_COL_INV, s);
   return cudaGetLastError();
 }
@@ -618,7 +626,8 @@ static int l21_variant() {
 
 // Mid-size variants (AGK_MVAR) for 2^14 <= P <= 2^20: fewer points per thread = more warps.
 #define AGK_MID_VARIANTS(X, L) \
-  X(1, L, 8, 8, 4) X(2, L, 4, 4, 4) X(3, L, 4, 8, 8) X(4, L, 8, 8, 8)
+  X(1, L, 8, 8, 4, 8) X(2, L, 4, 4, 4, 4) X(3, L, 4, 8, 8, 4) X(4, L, 8, 8, 8, 8) X(5, L, 8, 8, 4, 4) X(6, L, 8, 4, 4, 4) \
+  X(7, L, 4, 8, 4, 4) X(8, L, 8, 8, 8, 4) X(9, L, 8, 8, 2, 4) X(10, L, 8, 8, 4, 2) X(11, L, 8, 8, 4, 8)
 
 static int mid_variant() {
   static int v = -1;
@@ -633,10 +642,10 @@ static int mid_variant() {
 template <int L>
 static cudaError_t launch_four_step(const RhsPlan& p, const RhsArgs& a, cudaStream_t s, Marks* mk) {
 #ifdef AGK_EXPERIMENTS
-  if constexpr (L >= 16 && L <= 20) {
+  if constexpr (L >= 14 && L <= 20) {
     switch (mid_variant()) {
-#define AGK_M(id, LL, e1, e2, c) \
-  case id: return launch_four_step_cf<Cfg<LL, e1, e2, c, 0>>(p, a, s, mk);
+#define AGK_M(id, LL, e1, e2, c, e1i) \
+  case id: return launch_four_step_cf<Cfg<LL, e1, e2, c, 0, e1i>>(p, a, s, mk);
       AGK_MID_VARIANTS(AGK_M, L)
 #undef AGK_M
       default: break;
@@ -711,7 +720,7 @@ static cudaError_t smem_four_step_cf() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_row<CF::N2, CF::E2, CF::ROW_STAGE, CF::ROW_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SM_ROW);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_col_inv<CF::N1, CF::E1I, CF::CP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)CF::SM_COLINV);
 }
 
@@ -726,9 +735,9 @@ static cudaError_t smem_four_step() {
     AGK_L21_VARIANTS(AGK_X)
 #undef AGK_X
   }
-  if constexpr (L >= 16 && L <= 20) {
-#define AGK_M(id, LL, e1, e2, c) \
-  if ((e = smem_four_step_cf<Cfg<LL, e1, e2, c, 0>>()) != cudaSuccess) return e;
+  if constexpr (L >= 14 && L <= 20) {
+#define AGK_M(id, LL, e1, e2, c, e1i) \
+  if ((e = smem_four_step_cf<Cfg<LL, e1, e2, c, 0, e1i>>()) != cudaSuccess) return e;
     AGK_MID_VARIANTS(AGK_M, L)
 #undef AGK_M
   }
