@@ -10,6 +10,7 @@ Cases ("Next round" item 1):
     R_f = 2 (k_dvec after the row pass) and with R_f = 16 (k_dvec beside it); R_f = 20 (two rank
     groups: the accumulating row launch);
   * the m in (2^20, 2^22] four-step paths (P = 2^22, 2^23): m = 2^20 + 1, 3 * 2^20, 2^22;
+  * the four-step path at P = 2^18, 2^19, 2^20 (m = 100001, 200001, 400001, 2^19);
   * one RKF45 `advance` (the device trial loop + controller) at config 5 full shape.
 Bar: north_star's 1e-11 max normwise relative error per RHS, exact zeros where the reference
 has them. Measured values are appended to $AGK_PARITY_REPORT (JSON lines) when it is set.
@@ -104,6 +105,17 @@ def test_warp_path_odd_sizes(agk, ref, m):
     check(f"warp_m{m}_rf2", agk, ref, u, v, O.SOURCES, [(1, 1.0), (7, 0.5)], 0.0, cfg5_state(m, rng), want_rf=2)
     U, V, n = config4_inputs(m, 16)
     check(f"warp_m{m}_rf16_shatter", agk, ref, U, V, O.SHATTERING, [], 0.01, n, want_rf=16)
+
+
+@pytest.mark.parametrize("m", [100001, 200001, 400001, 1 << 19])
+def test_mid_four_step_sizes(agk, ref, m):
+    """The four-step path between the config-3 shape and the warp path (P = 2^18, 2^19, 2^20: 8 points
+    per thread in the forward column and row passes), odd sizes included."""
+    rng = np.random.default_rng(m)
+    u, v = factors("brownian2", m)
+    check(f"mid_m{m}_rf2", agk, ref, u, v, O.SOURCES, [(1, 1.0), (5, 0.25)], 0.0, cfg5_state(m, rng), want_rf=2)
+    u, v = factors("brownian", m, 0.9)
+    check(f"mid_m{m}_shatter", agk, ref, u, v, O.SHATTERING, [], 0.01, cfg3_state(m, rng), want_rf=1)
 
 
 def test_warp_path_two_rank_groups(agk, ref):
